@@ -1,0 +1,71 @@
+"""Build recipe for the product library (sm_100a only) and the test checkers.
+
+    python -m paper_1909_07717_b200.build          # product + checkers
+
+The product is ONE shared library, lib/libpassplan_b200.so, exporting the
+C-ABI of include/passplan_b200.h.  Host code is compiled with
+-ffp-contract=off (the reference's rule, proj/CMakeLists.txt:12-14).
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB_DIR = os.path.join(PKG, "lib")
+LIB = os.path.join(LIB_DIR, "libpassplan_b200.so")
+DROPIN_LIB = os.path.join(LIB_DIR, "libpassplan.so")
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _run(cmd, cwd=None):
+    print("+", " ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True, cwd=cwd)
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_product(force: bool = False, verbose_ptxas: bool = False) -> str:
+    os.makedirs(LIB_DIR, exist_ok=True)
+    srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC))
+            if f.endswith((".cu", ".cuh", ".h", ".hpp"))]
+    hdrs = [os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))
+            if f.endswith(".h")]
+    if force or _stale(LIB, srcs + hdrs):
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17",
+               "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-shared",
+               "-I", os.path.join(ROOT, "include"), "-o", LIB,
+               os.path.join(CSRC, "pp_cabi.cu")]
+        if verbose_ptxas:
+            cmd.insert(1, "-Xptxas=-v")
+        _run(cmd)
+    return LIB
+
+
+def build_checkers() -> None:
+    """oracle/liboracle.so always; oracle/_ref/ when the reference tree exists
+    (this container).  The GPU box only uses the prebuilt files."""
+    oracle_dir = os.path.join(ROOT, "oracle")
+    if os.path.exists(os.path.join(oracle_dir, "pp_oracle.c")):
+        _run(["make", "-s", "-C", oracle_dir, f"PY={sys.executable}", "liboracle.so"])
+    if os.path.isdir("/root/reference/proj/src"):
+        _run(["make", "-s", "-j8", "-C", oracle_dir, f"PY={sys.executable}", "ref"])
+
+
+def build_all(force: bool = False) -> None:
+    build_product(force=force)
+    build_checkers()
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)

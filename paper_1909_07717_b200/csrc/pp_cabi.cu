@@ -1,0 +1,963 @@
+// pp_cabi.cu -- host side of the C-ABI declared in include/passplan_b200.h.
+//
+// Owns validation (config.cpp:172-200, dpps.cpp:22-28, 219-223), the staging
+// of world state into the kernels' FrameDev layout (id-sorted teams,
+// dpps.cpp:79-92), the direction table (dpps.cpp:30-48, computed here with the
+// host libm so it is bit-identical to the reference's), and the launches.
+// Host code is compiled with -ffp-contract=off like the reference.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "passplan_b200.h"
+#include "passplan_b200_layout.h"
+#include "pp_kernels.cuh"
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;  // == std::numbers::pi
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t reserve(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) {
+      bytes = want;
+      e = cudaMemset(p, 0, want);
+    }
+    return e;
+  }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  cudaError_t reserve(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocDefault);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+};
+
+}  // namespace
+
+struct pp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::string err;
+  // single frame
+  DevBuf frame, block, partials, counters, dirs, scratch_in, scratch_out;
+  PinnedBuf frame_h;
+  int dirs_n = -1;
+  // run map
+  DevBuf run_block, run_partials, run_counter;
+  // batch
+  DevBuf batch_frames, batch_sums;
+  std::vector<pp::FrameDev> batch_host;
+  std::vector<int32_t> batch_kickers, batch_poss;
+  int64_t batch_n = 0;
+};
+
+namespace {
+
+pp_status fail(pp_ctx* ctx, pp_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  return st;
+}
+
+#define PP_CUDA_TRY(ctx, expr)                                                              \
+  do {                                                                                      \
+    const cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail((ctx), PP_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                                \
+  } while (0)
+
+void put(char* msg, size_t len, const std::string& s) {
+  if (msg && len) std::snprintf(msg, len, "%s", s.c_str());
+}
+
+// PlannerConfig::validate (config.cpp:172-200) minus SvgStyle, plus
+// BallModelParams/MotionLimits::validate (ball_model.cpp:47-60, motion.cpp:10-14)
+// and SearchGrid::validate (dpps.cpp:22-28).
+bool validate_params(const pp_params& p, std::string* why) {
+  const pp_ball_model& b = p.ball;
+  if (!(b.slide_decel > b.roll_decel) || !(b.roll_decel > 0.0)) {
+    *why = "ball model requires slide_decel > roll_decel > 0";
+    return false;
+  }
+  if (!(b.transition_ratio > 0.0) || !(b.transition_ratio < 1.0)) {
+    *why = "transition_ratio must lie in (0,1)";
+    return false;
+  }
+  if (!(b.power_min > 0.0) || !(b.power_min < b.power_max)) {
+    *why = "ball model requires 0 < power_min < power_max";
+    return false;
+  }
+  if (!(b.chip_flight_fraction > 0.0) || !(b.chip_flight_fraction < 1.0)) {
+    *why = "chip_flight_fraction must lie in (0,1)";
+    return false;
+  }
+  for (const pp_motion_limits* m : {&p.motion_ours, &p.motion_theirs}) {
+    if (!(m->max_speed > 0.0) || !(m->max_accel > 0.0) || !(m->max_decel > 0.0)) {
+      *why = "motion limits must all be positive";
+      return false;
+    }
+  }
+  const pp_search_grid& g = p.grid;
+  if (g.n_directions < 1) {
+    *why = "grid.n_directions must be >= 1";
+    return false;
+  }
+  if (g.n_powers < 1) {
+    *why = "grid.n_powers must be >= 1";
+    return false;
+  }
+  if (!(g.power_min > 0.0) || !(g.power_min <= g.power_max)) {
+    *why = "grid requires 0 < power_min <= power_max";
+    return false;
+  }
+  const pp_thresholds& t = p.thresholds;
+  struct Rule {
+    bool ok;
+    const char* msg;
+  };
+  const Rule rules[] = {
+      {t.sbip_dt > 0.0, "thresholds.sbip_dt must be > 0"},
+      {t.possession_dt > 0.0, "thresholds.possession_dt must be > 0"},
+      {t.robot_radius >= 0.0, "thresholds.robot_radius must be >= 0"},
+      {t.safety_margin >= 0.0, "thresholds.safety_margin must be >= 0"},
+      {t.buffer_time >= 0.0, "thresholds.buffer_time must be >= 0"},
+      {t.possession_radius > 0.0, "thresholds.possession_radius must be > 0"},
+      {t.angle_threshold >= 0.0, "thresholds.angle_threshold must be >= 0"},
+      {t.shot_power >= 0.0, "thresholds.shot_power must be >= 0"},
+      {t.margin_cap > 0.0, "thresholds.margin_cap must be > 0"},
+      {t.contest_epsilon >= 0.0, "thresholds.contest_epsilon must be >= 0"},
+      {t.grid_step > 0.0, "thresholds.grid_step must be > 0"},
+      {t.min_zone_width > 0.0, "thresholds.min_zone_width must be > 0"},
+      {t.guard_time_cap > 0.0, "thresholds.guard_time_cap must be > 0"},
+      {t.drag_v_min >= 0.0, "thresholds.drag_v_min must be >= 0"},
+      {t.marking_radius > 0.0, "thresholds.marking_radius must be > 0"},
+      {p.norm.length_upper >= 0.0, "norm.length_upper must be >= 0"},
+      {p.norm.angle_upper > 0.0, "norm.angle_upper must be > 0"},
+  };
+  for (const Rule& r : rules) {
+    if (!r.ok) {
+      *why = r.msg;
+      return false;
+    }
+  }
+  const pp_angle_band& a = p.angle_band;
+  if (!(a.full_lo <= a.peak_lo && a.peak_lo <= a.peak_hi && a.peak_hi <= a.full_hi)) {
+    *why = "angle_band knots must be non-decreasing";
+    return false;
+  }
+  return true;
+}
+
+bool validate_grid(const pp_search_grid& g, std::string* why) {
+  if (g.n_directions < 1) {
+    *why = "grid.n_directions must be >= 1";
+    return false;
+  }
+  if (g.n_powers < 1) {
+    *why = "grid.n_powers must be >= 1";
+    return false;
+  }
+  if (!(g.power_min > 0.0) || !(g.power_min <= g.power_max)) {
+    *why = "grid requires 0 < power_min <= power_max";
+    return false;
+  }
+  return true;
+}
+
+// direction_table (dpps.cpp:30-48) with the host libm, bit-identical.
+std::vector<double> direction_table(int n) {
+  std::vector<double> xy(2 * static_cast<size_t>(n));
+  for (int k = 0; k <= n / 2; ++k) {
+    const double theta = -kPi + k * (2.0 * kPi / n);
+    double c = std::cos(theta);
+    double s = std::sin(theta);
+    if (k == 0) {
+      c = -1.0;
+      s = 0.0;
+    }
+    xy[2 * k] = c;
+    xy[2 * k + 1] = s;
+    const int m = (n - k) % n;
+    if (m != k) {
+      xy[2 * m] = c;
+      xy[2 * m + 1] = -s;
+    }
+  }
+  return xy;
+}
+
+// Team slots in id order (dpps.cpp:79-92; stable for equal ids).
+std::vector<int> id_order(const pp_robot* robots, int n) {
+  std::vector<int> idx(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) idx[i] = i;
+  std::stable_sort(idx.begin(), idx.end(),
+                   [&](int a, int b) { return robots[a].id < robots[b].id; });
+  return idx;
+}
+
+// Stages one world into FrameDev.  Returns false (validation) when the kicker
+// is not on team ours (dpps.cpp:221-223).
+bool pack_frame(const pp_world& w, int32_t kicker_id, pp::FrameDev* F, int32_t* kicker_slot_out,
+                std::string* why) {
+  std::memset(F, 0, sizeof(*F));
+  if (w.n_ours < 0 || w.n_ours > PP_MAX_TEAM || w.n_theirs < 0 || w.n_theirs > PP_MAX_TEAM) {
+    *why = "team size outside [0, 16]";
+    return false;
+  }
+  bool found = false;
+  for (int i = 0; i < w.n_ours; ++i) found = found || w.ours[i].id == kicker_id;
+  if (!found) {
+    *why = "kicker id " + std::to_string(kicker_id) + " is not on team ours";
+    return false;
+  }
+  const std::vector<int> so = id_order(w.ours, w.n_ours);
+  const std::vector<int> st = id_order(w.theirs, w.n_theirs);
+  int kicker_slot = -1;
+  for (int s = 0; s < w.n_ours; ++s) {
+    const pp_robot& r = w.ours[so[s]];
+    F->px[s] = r.px;
+    F->py[s] = r.py;
+    F->vx[s] = r.vx;
+    F->vy[s] = r.vy;
+    F->id[s] = r.id;
+    if (r.id == kicker_id) kicker_slot = s;  // last match, like dpps.cpp:250-252
+  }
+  for (int s = 0; s < w.n_theirs; ++s) {
+    const pp_robot& r = w.theirs[st[s]];
+    F->px[pp::kTheirs + s] = r.px;
+    F->py[pp::kTheirs + s] = r.py;
+    F->vx[pp::kTheirs + s] = r.vx;
+    F->vy[pp::kTheirs + s] = r.vy;
+    F->id[pp::kTheirs + s] = r.id;
+  }
+  F->ball_x = w.ball_px;
+  F->ball_y = w.ball_py;
+  F->L = w.field.length;
+  F->W = w.field.width;
+  F->gw = w.field.goal_width;
+  F->dd = w.field.defense_depth;
+  F->dw = w.field.defense_width;
+  F->n_ours = w.n_ours;
+  F->n_theirs = w.n_theirs;
+  F->kicker_slot = kicker_slot;
+  int n = 0;
+  for (int s = 0; s < w.n_ours; ++s)
+    if (s != kicker_slot) F->scan_slot[n++] = static_cast<int8_t>(s);
+  for (int s = 0; s < w.n_theirs; ++s) F->scan_slot[n++] = static_cast<int8_t>(pp::kTheirs + s);
+  F->n_scan = n;
+  *kicker_slot_out = kicker_slot;
+  return true;
+}
+
+const pp_robot* find_ours(const pp_world& w, int32_t id) {
+  for (int i = 0; i < w.n_ours; ++i)
+    if (w.ours[i].id == id) return &w.ours[i];
+  return nullptr;
+}
+
+double host_distance(double ax, double ay, double bx, double by) {
+  const double dx = ax - bx, dy = ay - by;
+  return std::sqrt(dx * dx + dy * dy);
+}
+
+pp::DevParams make_dev_params(const pp_params& p, const pp_search_grid& g) {
+  pp::DevParams d{};
+  d.slide = p.ball.slide_decel;
+  d.roll = p.ball.roll_decel;
+  d.ratio = p.ball.transition_ratio;
+  d.chip_frac = p.ball.chip_flight_fraction;
+  d.dt = p.thresholds.sbip_dt;
+  d.radius = p.thresholds.robot_radius;
+  d.safety = p.thresholds.safety_margin;
+  d.margin_cap = p.thresholds.margin_cap;
+  d.a_o = p.motion_ours.max_accel;
+  d.b_o = p.motion_ours.max_decel;
+  d.vmax_o = p.motion_ours.max_speed;
+  d.a_t = p.motion_theirs.max_accel;
+  d.b_t = p.motion_theirs.max_decel;
+  d.vmax_t = p.motion_theirs.max_speed;
+  d.pw_t = p.pass_weights.teammate_time;
+  d.pw_s = p.pass_weights.shoot_angle;
+  d.pw_d = p.pass_weights.dist_goal;
+  d.pw_r = p.pass_weights.refraction;
+  d.pw_m = p.pass_weights.margin;
+  d.len_upper_cfg = p.norm.length_upper;
+  d.ang_upper = p.norm.angle_upper;
+  d.power_min = g.power_min;
+  d.power_max = g.power_max;
+  d.n_dirs = g.n_directions;
+  d.n_pows = g.n_powers;
+  d.n_kt = (g.flat ? 1 : 0) + (g.chip ? 1 : 0);
+  d.kt_chip0 = g.flat ? 0 : 1;
+  d.kt_chip1 = 1;
+  d.n_ptiles = (g.n_powers + 31) / 32;
+  d.n_tiles = d.n_kt * g.n_directions * d.n_ptiles;
+  return d;
+}
+
+void fill_summary_host(pp_dpps_summary* s, const pp_world& w, const pp_search_grid& g,
+                       int32_t kicker_id, int32_t kicker_slot, int32_t possession) {
+  s->n_cells = pp_grid_cells(&g);
+  s->n_kick_types = (g.flat ? 1 : 0) + (g.chip ? 1 : 0);
+  s->kick_types[0] = g.flat ? 0 : 1;
+  s->kick_types[1] = 1;
+  s->n_directions = g.n_directions;
+  s->n_powers = g.n_powers;
+  s->kicker_id = kicker_id;
+  s->kicker_slot = kicker_slot;
+  s->kicker_in_possession = possession;
+  s->n_ours = w.n_ours;
+  s->n_theirs = w.n_theirs;
+  const std::vector<int> so = id_order(w.ours, w.n_ours);
+  const std::vector<int> st = id_order(w.theirs, w.n_theirs);
+  for (int i = 0; i < PP_MAX_TEAM; ++i) {
+    s->ours_ids[i] = i < w.n_ours ? w.ours[so[i]].id : -1;
+    s->theirs_ids[i] = i < w.n_theirs ? w.theirs[st[i]].id : -1;
+  }
+  s->sbip_calls = static_cast<uint64_t>(s->n_cells) *
+                  static_cast<uint64_t>(w.n_ours + w.n_theirs);  // dpps.cpp:148-153
+}
+
+int32_t possession_of(const pp_world& w, int32_t kicker_id, const pp_params& p) {
+  const pp_robot* k = find_ours(w, kicker_id);
+  if (!k) return 0;
+  return host_distance(w.ball_px, w.ball_py, k->px, k->py) <= p.thresholds.possession_radius;
+}
+
+cudaError_t ensure_dirs(pp_ctx* ctx, int n) {
+  if (ctx->dirs_n == n) return cudaSuccess;
+  const std::vector<double> xy = direction_table(n);
+  cudaError_t e = ctx->dirs.reserve(xy.size() * sizeof(double));
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpy(ctx->dirs.p, xy.data(), xy.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) ctx->dirs_n = n;
+  return e;
+}
+
+int warps_for(int n_scan) {
+  int w = n_scan < 4 ? 4 : n_scan;
+  return w > 16 ? 16 : w;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pp_abi_version(void) { return PP_ABI_VERSION; }
+const char* pp_kernel_name(void) { return "sm100a"; }
+
+void pp_params_default(pp_params* p) {
+  std::memset(p, 0, sizeof(*p));
+  p->ball = {3.4, 0.5, 5.0 / 7.0, 1.0, 6.5, 0.5};
+  p->motion_ours = {3.25, 3.0, 3.0};
+  p->motion_theirs = {3.25, 3.0, 3.0};
+  p->grid = {128, 64, 1.0, 6.5, 1, 1};
+  p->pass_weights = {1.0, 2.0, 1.0, 0.5, 1.0};
+  p->run_weights = {1.0, 0.3, 1.0, 0.3, 0.5};
+  p->norm = {0.0, kPi};
+  p->angle_band = {0.0, 15.0 * kPi / 180.0, 45.0 * kPi / 180.0, 90.0 * kPi / 180.0};
+  p->thresholds = {1.0 / 60.0, 0.09, 0.3, 0.3, 0.15, 0.1, 0.0, 10.0,
+                   1e-3,       1e-3, 0.1, 1.0, 10.0, 1.0, 0.6};
+}
+
+pp_status pp_params_validate(const pp_params* params, char* msg, size_t msg_len) {
+  std::string why;
+  if (!params) {
+    put(msg, msg_len, "null params");
+    return PP_INTERNAL;
+  }
+  if (!validate_params(*params, &why)) {
+    put(msg, msg_len, why);
+    return PP_CONFIG;
+  }
+  return PP_OK;
+}
+
+size_t pp_grid_bytes(int64_t n_cells) { return pp_grid_offsets_for_(n_cells).total; }
+void pp_grid_view_of(void* block, int64_t n_cells, pp_grid_view* out) {
+  pp_grid_view_of_(block, n_cells, out);
+}
+size_t pp_runmap_bytes(int64_t n_vertices) { return pp_runmap_offsets_for_(n_vertices).total; }
+void pp_runmap_view_of(void* block, int64_t n_vertices, pp_runmap_view* out) {
+  pp_runmap_view_of_(block, n_vertices, out);
+}
+
+int64_t pp_grid_cells(const pp_search_grid* g) {
+  if (!g || g->n_directions < 1 || g->n_powers < 1) return 0;
+  return static_cast<int64_t>((g->flat ? 1 : 0) + (g->chip ? 1 : 0)) * g->n_directions *
+         g->n_powers;
+}
+
+void* pp_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+  return p;
+}
+void pp_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+pp_status pp_ctx_create(int device, pp_ctx** out) {
+  if (!out) return PP_INTERNAL;
+  *out = nullptr;
+  std::unique_ptr<pp_ctx> ctx(new pp_ctx());
+  ctx->device = device;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device || device < 0)
+    return PP_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return PP_CUDA;
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return PP_CUDA;
+  if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess)
+    return PP_CUDA;
+  if (ctx->frame.reserve(sizeof(pp::FrameDev)) != cudaSuccess) return PP_CUDA;
+  if (ctx->frame_h.reserve(sizeof(pp::FrameDev)) != cudaSuccess) return PP_CUDA;
+  *out = ctx.release();
+  return PP_OK;
+}
+
+void pp_ctx_destroy(pp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* pp_last_error(const pp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
+                  const pp_search_grid* grid_in, int32_t kicker_id, uint32_t copy_flags,
+                  void* block) {
+  if (!ctx || !world || !params || !block) return fail(ctx, PP_INTERNAL, "null argument");
+  ctx->err.clear();
+  const pp_search_grid& g = grid_in ? *grid_in : params->grid;
+  std::string why;
+  if (!validate_grid(g, &why)) return fail(ctx, PP_CONFIG, "%s", why.c_str());
+  if (!validate_params(*params, &why)) return fail(ctx, PP_CONFIG, "%s", why.c_str());
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  pp::FrameDev* F = static_cast<pp::FrameDev*>(ctx->frame_h.p);
+  int32_t kicker_slot = -1;
+  if (!pack_frame(*world, kicker_id, F, &kicker_slot, &why))
+    return fail(ctx, PP_VALIDATION, "%s", why.c_str());
+
+  const int64_t n_cells = pp_grid_cells(&g);
+  const pp_grid_offsets_ off = pp_grid_offsets_for_(n_cells);
+  pp_grid_view hv;
+  pp_grid_view_of_(block, n_cells, &hv);
+  if (n_cells == 0) {
+    std::memset(hv.summary, 0, sizeof(pp_dpps_summary));
+    for (int k = 0; k < 3; ++k) hv.summary->best_cell[k] = -1;
+    fill_summary_host(hv.summary, *world, g, kicker_id, kicker_slot,
+                      possession_of(*world, kicker_id, *params));
+    return PP_OK;
+  }
+  const pp::DevParams P = make_dev_params(*params, g);
+  PP_CUDA_TRY(ctx, ensure_dirs(ctx, g.n_directions));
+  PP_CUDA_TRY(ctx, ctx->block.reserve(off.total));
+  PP_CUDA_TRY(ctx, ctx->partials.reserve(sizeof(pp::Partial) * static_cast<size_t>(P.n_tiles)));
+  PP_CUDA_TRY(ctx, ctx->counters.reserve(sizeof(unsigned) * 4));
+
+  char* dblk = static_cast<char*>(ctx->block.p);
+  pp::CellOut co;
+  co.our_time = reinterpret_cast<double*>(dblk + off.our_time);
+  co.opp_time = reinterpret_cast<double*>(dblk + off.opp_time);
+  co.rx = reinterpret_cast<double*>(dblk + off.rx);
+  co.ry = reinterpret_cast<double*>(dblk + off.ry);
+  co.score = reinterpret_cast<float*>(dblk + off.score);
+  co.our_slot = reinterpret_cast<int8_t*>(dblk + off.our_slot);
+  co.opp_slot = reinterpret_cast<int8_t*>(dblk + off.opp_slot);
+  co.feasible = reinterpret_cast<uint8_t*>(dblk + off.feasible);
+  pp_dpps_summary* dsum = reinterpret_cast<pp_dpps_summary*>(dblk + off.summary);
+
+  cudaStream_t s = ctx->stream;
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->frame.p, F, sizeof(pp::FrameDev), cudaMemcpyHostToDevice, s));
+  PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, s));
+  const int threads = 32 * warps_for(F->n_scan);
+  pp::dpps_kernel<true><<<P.n_tiles, threads, 0, s>>>(
+      static_cast<const pp::FrameDev*>(ctx->frame.p), static_cast<const double2*>(ctx->dirs.p), P,
+      P.n_tiles, 1, co, static_cast<pp::Partial*>(ctx->partials.p),
+      static_cast<unsigned*>(ctx->counters.p), dsum);
+  PP_CUDA_TRY(ctx, cudaGetLastError());
+  PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, s));
+  const size_t bytes = (copy_flags & PP_COPY_ALL) ? off.total : sizeof(pp_dpps_summary);
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(block, dblk, bytes, cudaMemcpyDeviceToHost, s));
+  PP_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  fill_summary_host(hv.summary, *world, g, kicker_id, kicker_slot,
+                    possession_of(*world, kicker_id, *params));
+  hv.summary->device_ms = ms;
+  return PP_OK;
+}
+
+pp_status pp_score_cells(pp_ctx* ctx, const pp_world* world, const pp_params* params, int64_t n,
+                         const double* rx, const double* ry, const double* our_time,
+                         const double* opp_time, const uint8_t* feasible, double* score_out,
+                         pp_pass_features* features_out) {
+  if (!ctx || !world || !params) return fail(ctx, PP_INTERNAL, "null argument");
+  ctx->err.clear();
+  for (int64_t i = 0; i < n; ++i)
+    if (!feasible[i]) return fail(ctx, PP_DOMAIN, "score_pass: candidate is not feasible");
+  if (n == 0) return PP_OK;
+  std::string why;
+  if (!validate_params(*params, &why)) return fail(ctx, PP_CONFIG, "%s", why.c_str());
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  pp::FrameDev* F = static_cast<pp::FrameDev*>(ctx->frame_h.p);
+  int32_t ks = -1;
+  pp_world w = *world;
+  if (w.n_ours == 0) {  // score_pass needs no kicker; stage a placeholder
+    w.n_ours = 1;
+    w.ours[0] = pp_robot{0, 0, 0, 0, 0, 0, 0};
+  }
+  if (!pack_frame(w, w.ours[0].id, F, &ks, &why)) return fail(ctx, PP_VALIDATION, "%s", why.c_str());
+  const pp::DevParams P = make_dev_params(*params, params->grid);
+  std::vector<double> in(4 * static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    in[4 * i] = rx[i];
+    in[4 * i + 1] = ry[i];
+    in[4 * i + 2] = our_time[i];
+    in[4 * i + 3] = opp_time[i];
+  }
+  PP_CUDA_TRY(ctx, ctx->scratch_in.reserve(in.size() * 8));
+  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(6 * static_cast<size_t>(n) * 8));
+  cudaStream_t s = ctx->stream;
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->frame.p, F, sizeof(pp::FrameDev), cudaMemcpyHostToDevice, s));
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->scratch_in.p, in.data(), in.size() * 8, cudaMemcpyHostToDevice, s));
+  const int blocks = static_cast<int>((n + 7) / 8);
+  pp::score_cells_kernel<<<blocks, 256, 0, s>>>(static_cast<const pp::FrameDev*>(ctx->frame.p), P,
+                                                n, static_cast<const double*>(ctx->scratch_in.p),
+                                                static_cast<double*>(ctx->scratch_out.p));
+  PP_CUDA_TRY(ctx, cudaGetLastError());
+  std::vector<double> o(6 * static_cast<size_t>(n));
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(o.data(), ctx->scratch_out.p, o.size() * 8, cudaMemcpyDeviceToHost, s));
+  PP_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < n; ++i) {
+    score_out[i] = o[6 * i];
+    if (features_out)
+      features_out[i] = pp_pass_features{o[6 * i + 1], o[6 * i + 2], o[6 * i + 3], o[6 * i + 4],
+                                         o[6 * i + 5]};
+  }
+  return PP_OK;
+}
+
+pp_status pp_goal_views(pp_ctx* ctx, const pp_world* world, double robot_radius, int64_t n,
+                        const double* px, const double* py, double* angle, double* window_lo,
+                        double* window_hi, double* target_y) {
+  if (!ctx || !world) return fail(ctx, PP_INTERNAL, "null argument");
+  ctx->err.clear();
+  if (n == 0) return PP_OK;
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  pp::FrameDev* F = static_cast<pp::FrameDev*>(ctx->frame_h.p);
+  pp_world w = *world;
+  if (w.n_ours == 0) {
+    w.n_ours = 1;
+    w.ours[0] = pp_robot{0, 0, 0, 0, 0, 0, 0};
+  }
+  int32_t ks = -1;
+  std::string why;
+  if (!pack_frame(w, w.ours[0].id, F, &ks, &why)) return fail(ctx, PP_VALIDATION, "%s", why.c_str());
+  std::vector<double> in(2 * static_cast<size_t>(n));
+  std::memcpy(in.data(), px, n * 8);
+  std::memcpy(in.data() + n, py, n * 8);
+  PP_CUDA_TRY(ctx, ctx->scratch_in.reserve(in.size() * 8));
+  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(4 * static_cast<size_t>(n) * 8));
+  cudaStream_t s = ctx->stream;
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->frame.p, F, sizeof(pp::FrameDev), cudaMemcpyHostToDevice, s));
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->scratch_in.p, in.data(), in.size() * 8, cudaMemcpyHostToDevice, s));
+  const double* dpx = static_cast<const double*>(ctx->scratch_in.p);
+  pp::goal_view_kernel<<<static_cast<int>((n + 7) / 8), 256, 0, s>>>(
+      static_cast<const pp::FrameDev*>(ctx->frame.p), robot_radius, n, dpx, dpx + n,
+      static_cast<double*>(ctx->scratch_out.p));
+  PP_CUDA_TRY(ctx, cudaGetLastError());
+  std::vector<double> o(4 * static_cast<size_t>(n));
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(o.data(), ctx->scratch_out.p, o.size() * 8, cudaMemcpyDeviceToHost, s));
+  PP_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < n; ++i) {
+    angle[i] = o[4 * i];
+    window_lo[i] = o[4 * i + 1];
+    window_hi[i] = o[4 * i + 2];
+    target_y[i] = o[4 * i + 3];
+  }
+  return PP_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Running-point map host side (offball.cpp:69-123, 137-174, 215-258).
+
+namespace {
+
+struct HostZone {
+  double x0, x1, y0, y1;
+};
+
+int axis_count(double span, double step) {
+  const int n = static_cast<int>(std::floor(span / step + 1e-9)) + 1;
+  return n > 0 ? n : 0;
+}
+
+double clampd(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
+
+struct RunSetup {
+  pp::RunParams R;
+  double cut_x, cut_y;
+  int64_t n_map;
+};
+
+bool setup_runmap(const pp_world& w, const pp_params& p, const pp_runmap_request& req,
+                  RunSetup* out, std::string* why) {
+  const pp_field& f = w.field;
+  const double mzw = p.thresholds.min_zone_width;
+  if (!(mzw > 0.0) || 2.0 * mzw > f.width) {
+    *why = "min_zone_width must be positive and at most half the field width";
+    return false;
+  }
+  const double step = p.thresholds.grid_step;
+  if (!(step > 0.0)) {
+    *why = "lattice step must be positive";
+    return false;
+  }
+  pp::RunParams& R = out->R;
+  std::memset(&R, 0, sizeof(R));
+  const double cut_x = 0.25 * f.length;
+  const double cut_y = clampd(w.ball_py, -0.5 * f.width + mzw, 0.5 * f.width - mzw);
+  const double x_mid = 0.5 * f.length;
+  const double y_top = 0.5 * f.width;
+  const HostZone zones[4] = {{0.0, cut_x, cut_y, y_top},
+                             {0.0, cut_x, -y_top, cut_y},
+                             {cut_x, x_mid, cut_y, y_top},
+                             {cut_x, x_mid, -y_top, cut_y}};
+  out->cut_x = cut_x;
+  out->cut_y = cut_y;
+  // Zone selection (offball.cpp:221-233).
+  uint32_t excluded = req.occupied_mask;
+  if (req.has_best_pass_point) {
+    const double px = req.best_pass_px, py = req.best_pass_py;
+    const double x_lo = zones[0].x0, x_hi = zones[2].x1, y_lo = zones[1].y0, y_hi = zones[0].y1;
+    if (!(px < x_lo || px > x_hi || py < y_lo || py > y_hi)) {
+      const int z = px >= cut_x ? (py >= cut_y ? 2 : 3) : (py >= cut_y ? 0 : 1);
+      excluded |= 1u << z;
+    }
+  }
+  uint32_t selected = 0;
+  int n_sel = 0;
+  for (int z : {2, 3, 0, 1}) {
+    if (n_sel >= req.n_runners) break;
+    if (!(excluded & (1u << z))) {
+      selected |= 1u << z;
+      ++n_sel;
+    }
+  }
+  int64_t at = 0;
+  int max_blocks = 1;
+  for (int z = 0; z < 4; ++z) {
+    const HostZone& Z = zones[z];
+    pp::RunZone& rz = R.zone[z];
+    const bool upper = z == 0 || z == 2;
+    rz.x0 = Z.x0;
+    rz.y0 = upper ? Z.y0 : Z.y1;
+    rz.ydir = upper ? 1.0 : -1.0;
+    rz.nx = axis_count(Z.x1 - Z.x0, step);
+    rz.ny = axis_count(Z.y1 - Z.y0, step);
+    rz.selected = (selected >> z) & 1u;
+    rz.in_map = (req.zone_mask >> z) & 1u;
+    rz.offset = at;
+    if (rz.in_map) at += static_cast<int64_t>(rz.nx) * rz.ny;
+    const int64_t nv = static_cast<int64_t>(rz.nx) * rz.ny;
+    const int b = static_cast<int>((nv + 255) / 256);
+    R.blocks_per_zone[z] = (rz.in_map || rz.selected) ? b : 0;
+    if (R.blocks_per_zone[z] > max_blocks) max_blocks = R.blocks_per_zone[z];
+  }
+  out->n_map = at;
+  R.step = step;
+  R.L = f.length;
+  R.W = f.width;
+  R.dd = f.defense_depth;
+  R.dw = f.defense_width;
+  R.gw = f.goal_width;
+  R.ball_x = w.ball_px;
+  R.ball_y = w.ball_py;
+  R.a_t = p.motion_theirs.max_accel;
+  R.b_t = p.motion_theirs.max_decel;
+  R.vmax_t = p.motion_theirs.max_speed;
+  R.cap = p.thresholds.guard_time_cap;
+  R.w_dg = p.run_weights.dist_goal;
+  R.w_db = p.run_weights.dist_ball;
+  R.w_angle = p.run_weights.angle;
+  R.w_guard = p.run_weights.guard_time;
+  R.w_exp = p.run_weights.exposure;
+  R.len_upper = p.norm.length_upper > 0.0 ? p.norm.length_upper : f.length;
+  R.band_full_lo = p.angle_band.full_lo;
+  R.band_peak_lo = p.angle_band.peak_lo;
+  R.band_peak_hi = p.angle_band.peak_hi;
+  R.band_full_hi = p.angle_band.full_hi;
+  // Point-independent parts hoisted per frame: nearest opponent to the ball
+  // (offball.cpp:188-191) and the guard ranking (offball.cpp:143-155).
+  double nearest = std::numeric_limits<double>::infinity();
+  for (int i = 0; i < w.n_theirs; ++i) {
+    const double d = host_distance(w.theirs[i].px, w.theirs[i].py, w.ball_px, w.ball_py);
+    nearest = std::min(nearest, d);
+  }
+  R.nearest_opp = nearest;
+  const double bx0 = 0.5 * f.length - f.defense_depth, bx1 = 0.5 * f.length;
+  const double by0 = -0.5 * f.defense_width, by1 = 0.5 * f.defense_width;
+  struct Cand {
+    double dist;
+    int id;
+    int idx;
+  };
+  std::vector<Cand> cands;
+  for (int i = 0; i < w.n_theirs; ++i) {
+    const pp_robot& r = w.theirs[i];
+    const double cx = std::clamp(r.px, bx0, bx1);
+    const double cy = std::clamp(r.py, by0, by1);
+    cands.push_back({host_distance(r.px, r.py, cx, cy), r.id, i});
+  }
+  std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
+    if (a.dist != b.dist) return a.dist < b.dist;
+    return a.id < b.id;
+  });
+  R.n_guards = static_cast<int32_t>(std::min<size_t>(cands.size(), 2));
+  for (int g = 0; g < R.n_guards; ++g) {
+    const pp_robot& r = w.theirs[cands[g].idx];
+    R.g_px[g] = r.px;
+    R.g_py[g] = r.py;
+    R.g_vx[g] = r.vx;
+    R.g_vy[g] = r.vy;
+  }
+  (void)max_blocks;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+pp_status pp_runmap_count(const pp_world* world, const pp_params* params, uint32_t zone_mask,
+                          int64_t* n_vertices) {
+  if (!world || !params || !n_vertices) return PP_INTERNAL;
+  pp_runmap_request req{zone_mask, 0, 0, 0, 0.0, 0.0, 1};
+  RunSetup rs;
+  std::string why;
+  if (!setup_runmap(*world, *params, req, &rs, &why)) return PP_CONFIG;
+  *n_vertices = rs.n_map;
+  return PP_OK;
+}
+
+pp_status pp_runmap(pp_ctx* ctx, const pp_world* world, const pp_params* params,
+                    const pp_runmap_request* req, void* block, int64_t block_vertices) {
+  if (!ctx || !world || !params || !req || !block) return fail(ctx, PP_INTERNAL, "null argument");
+  ctx->err.clear();
+  std::string why;
+  if (!validate_params(*params, &why)) return fail(ctx, PP_CONFIG, "%s", why.c_str());
+  RunSetup rs;
+  if (!setup_runmap(*world, *params, *req, &rs, &why)) return fail(ctx, PP_CONFIG, "%s", why.c_str());
+  const bool want_map = req->want_map != 0;
+  const int64_t n_map = want_map ? rs.n_map : 0;
+  if (want_map && block_vertices < rs.n_map)
+    return fail(ctx, PP_INTERNAL, "runmap block holds %lld vertices, need %lld",
+                static_cast<long long>(block_vertices), static_cast<long long>(rs.n_map));
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const pp_runmap_offsets_ off = pp_runmap_offsets_for_(n_map);
+  PP_CUDA_TRY(ctx, ctx->run_block.reserve(off.total));
+  int max_blocks = 1;
+  for (int z = 0; z < 4; ++z) max_blocks = std::max(max_blocks, rs.R.blocks_per_zone[z]);
+  PP_CUDA_TRY(ctx, ctx->run_partials.reserve(sizeof(pp::RunPartial) * 4 * max_blocks));
+  PP_CUDA_TRY(ctx, ctx->run_counter.reserve(sizeof(unsigned) * 4));
+  char* d = static_cast<char*>(ctx->run_block.p);
+  pp::RunOut ro;
+  ro.px = reinterpret_cast<double*>(d + off.px);
+  ro.py = reinterpret_cast<double*>(d + off.py);
+  ro.score = reinterpret_cast<double*>(d + off.score);
+  ro.features = reinterpret_cast<pp_run_features*>(d + off.features);
+  ro.scorable = reinterpret_cast<uint8_t*>(d + off.scorable);
+  pp_runmap_summary* dsum = reinterpret_cast<pp_runmap_summary*>(d + off.summary);
+  cudaStream_t s = ctx->stream;
+  const dim3 grid(max_blocks, 4);
+  if (want_map) {
+    pp::runmap_kernel<true><<<grid, 256, 0, s>>>(rs.R, ro,
+                                                 static_cast<pp::RunPartial*>(ctx->run_partials.p),
+                                                 static_cast<unsigned*>(ctx->run_counter.p), dsum);
+  } else {
+    pp::runmap_kernel<false><<<grid, 256, 0, s>>>(rs.R, ro,
+                                                  static_cast<pp::RunPartial*>(ctx->run_partials.p),
+                                                  static_cast<unsigned*>(ctx->run_counter.p), dsum);
+  }
+  PP_CUDA_TRY(ctx, cudaGetLastError());
+  const size_t bytes = want_map ? off.total : sizeof(pp_runmap_summary);
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(block, d, bytes, cudaMemcpyDeviceToHost, s));
+  PP_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  pp_runmap_view v;
+  pp_runmap_view_of_(block, n_map, &v);
+  pp_runmap_summary& S = *v.summary;
+  S.cut_x = rs.cut_x;
+  S.cut_y = rs.cut_y;
+  S.n_vertices = n_map;
+  S.n_scorable = 0;
+  for (int z = 0; z < 4; ++z) {
+    const bool in_map = (req->zone_mask >> z) & 1u;
+    S.zone_nx[z] = in_map ? rs.R.zone[z].nx : 0;
+    S.zone_ny[z] = in_map ? rs.R.zone[z].ny : 0;
+    S.zone_offset[z] = rs.R.zone[z].offset;
+  }
+  if (want_map)
+    for (int64_t i = 0; i < n_map; ++i) S.n_scorable += v.scorable[i];
+  S.n_best = 0;
+  for (int z = 0; z < 4; ++z) {
+    S.best_order[z] = -1;
+    if (S.best[z].valid) S.best_order[S.n_best++] = z;
+  }
+  return PP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Batched frames: one CTA per frame, summaries only.
+
+pp_status pp_batch_upload(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
+                          const int32_t* kicker_ids) {
+  if (!ctx || (!frames && n_frames > 0)) return fail(ctx, PP_INTERNAL, "null argument");
+  ctx->err.clear();
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  ctx->batch_host.resize(static_cast<size_t>(n_frames));
+  ctx->batch_kickers.resize(static_cast<size_t>(n_frames));
+  for (int64_t i = 0; i < n_frames; ++i) {
+    const pp_world& w = frames[i];
+    int32_t kicker = -1;
+    if (kicker_ids) {
+      kicker = kicker_ids[i];
+    } else {  // nearest teammate, ties to the earlier entry
+      double best = std::numeric_limits<double>::infinity();
+      for (int r = 0; r < w.n_ours; ++r) {
+        const double d = host_distance(w.ours[r].px, w.ours[r].py, w.ball_px, w.ball_py);
+        if (d < best) {
+          best = d;
+          kicker = w.ours[r].id;
+        }
+      }
+    }
+    ctx->batch_kickers[i] = kicker;
+    int32_t ks = -1;
+    std::string why;
+    if (!pack_frame(w, kicker, &ctx->batch_host[i], &ks, &why))
+      return fail(ctx, PP_VALIDATION, "frame %lld: %s", static_cast<long long>(i), why.c_str());
+  }
+  ctx->batch_n = n_frames;
+  PP_CUDA_TRY(ctx, ctx->batch_frames.reserve(sizeof(pp::FrameDev) * std::max<int64_t>(n_frames, 1)));
+  PP_CUDA_TRY(ctx, cudaMemcpy(ctx->batch_frames.p, ctx->batch_host.data(),
+                              sizeof(pp::FrameDev) * n_frames, cudaMemcpyHostToDevice));
+  return PP_OK;
+}
+
+pp_status pp_batch_run(pp_ctx* ctx, const pp_params* params, const pp_search_grid* grid_in,
+                       float* device_ms) {
+  if (!ctx || !params) return fail(ctx, PP_INTERNAL, "null argument");
+  ctx->err.clear();
+  const pp_search_grid& g = grid_in ? *grid_in : params->grid;
+  std::string why;
+  if (!validate_grid(g, &why)) return fail(ctx, PP_CONFIG, "%s", why.c_str());
+  if (!validate_params(*params, &why)) return fail(ctx, PP_CONFIG, "%s", why.c_str());
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int64_t n = ctx->batch_n;
+  PP_CUDA_TRY(ctx, ctx->batch_sums.reserve(sizeof(pp_dpps_summary) * std::max<int64_t>(n, 1)));
+  if (n == 0 || pp_grid_cells(&g) == 0) {
+    if (device_ms) *device_ms = 0.f;
+    return PP_OK;
+  }
+  const pp::DevParams P = make_dev_params(*params, g);
+  PP_CUDA_TRY(ctx, ensure_dirs(ctx, g.n_directions));
+  int max_scan = 0;
+  for (const auto& F : ctx->batch_host) max_scan = std::max(max_scan, F.n_scan);
+  const int threads = 32 * warps_for(max_scan);
+  cudaStream_t s = ctx->stream;
+  pp::CellOut co{};
+  PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, s));
+  // Frames are independent: chunk the launch so gridDim.x stays moderate.
+  const int64_t chunk = 1 << 20;
+  for (int64_t f0 = 0; f0 < n; f0 += chunk) {
+    const int64_t nf = std::min(chunk, n - f0);
+    pp::dpps_kernel<false><<<static_cast<unsigned>(nf), threads, 0, s>>>(
+        static_cast<const pp::FrameDev*>(ctx->batch_frames.p) + f0,
+        static_cast<const double2*>(ctx->dirs.p), P, 1, P.n_tiles, co, nullptr, nullptr,
+        static_cast<pp_dpps_summary*>(ctx->batch_sums.p) + f0);
+    PP_CUDA_TRY(ctx, cudaGetLastError());
+  }
+  PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, s));
+  PP_CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  if (device_ms) *device_ms = ms;
+  return PP_OK;
+}
+
+pp_status pp_batch_download(pp_ctx* ctx, pp_dpps_summary* out) {
+  if (!ctx || (!out && ctx->batch_n > 0)) return fail(ctx, PP_INTERNAL, "null argument");
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int64_t n = ctx->batch_n;
+  if (n == 0) return PP_OK;
+  PP_CUDA_TRY(ctx, cudaMemcpy(out, ctx->batch_sums.p, sizeof(pp_dpps_summary) * n,
+                              cudaMemcpyDeviceToHost));
+  return PP_OK;
+}
+
+pp_status pp_dpps_batch(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
+                        const pp_params* params, const pp_search_grid* grid,
+                        const int32_t* kicker_ids, pp_dpps_summary* summaries) {
+  pp_status st = pp_batch_upload(ctx, frames, n_frames, kicker_ids);
+  if (st != PP_OK) return st;
+  st = pp_batch_run(ctx, params, grid, nullptr);
+  if (st != PP_OK) return st;
+  st = pp_batch_download(ctx, summaries);
+  if (st != PP_OK) return st;
+  const pp_search_grid& g = grid ? *grid : params->grid;
+  for (int64_t i = 0; i < n_frames; ++i) {
+    const int32_t k = ctx->batch_kickers[i];
+    const double dms = summaries[i].device_ms;
+    fill_summary_host(&summaries[i], frames[i], g, k, ctx->batch_host[i].kicker_slot,
+                      possession_of(frames[i], k, *params));
+    summaries[i].device_ms = dms;
+  }
+  return PP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,179 @@
+// pp_math.cuh -- device restatement of the reference's FP64 scalar math.
+//
+// The reference is compiled with -ffp-contract=off (proj/CMakeLists.txt:12-14):
+// every multiply and add rounds separately.  `xd` wraps a double whose
+// operators call the round-to-nearest intrinsics (__dadd_rn, __dmul_rn, ...),
+// which nvcc never fuses into DFMA, so each expression below rounds exactly
+// like the reference's.  IEEE add/sub/mul/div/sqrt are correctly rounded on
+// both sides, hence bit-identical results.  Only atan2 (goal view / run map)
+// is a libm call whose last ulp may differ from glibc; those feed scores,
+// which the parity bar compares at 1e-4 relative.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+namespace pp {
+
+struct xd {
+  double v;
+  __host__ __device__ __forceinline__ xd() : v(0.0) {}
+  __host__ __device__ __forceinline__ xd(double x) : v(x) {}  // NOLINT(implicit)
+};
+
+__device__ __forceinline__ xd operator+(xd a, xd b) { return __dadd_rn(a.v, b.v); }
+__device__ __forceinline__ xd operator-(xd a, xd b) { return __dsub_rn(a.v, b.v); }
+__device__ __forceinline__ xd operator*(xd a, xd b) { return __dmul_rn(a.v, b.v); }
+__device__ __forceinline__ xd operator/(xd a, xd b) { return __ddiv_rn(a.v, b.v); }
+__device__ __forceinline__ xd operator-(xd a) { return -a.v; }
+__device__ __forceinline__ bool operator<(xd a, xd b) { return a.v < b.v; }
+__device__ __forceinline__ bool operator>(xd a, xd b) { return a.v > b.v; }
+__device__ __forceinline__ bool operator<=(xd a, xd b) { return a.v <= b.v; }
+__device__ __forceinline__ bool operator>=(xd a, xd b) { return a.v >= b.v; }
+__device__ __forceinline__ bool operator==(xd a, xd b) { return a.v == b.v; }
+__device__ __forceinline__ xd xsqrt(xd a) { return __dsqrt_rn(a.v); }
+__device__ __forceinline__ xd xfabs(xd a) { return fabs(a.v); }
+
+// ---- vec2.hpp:22-56 ----------------------------------------------------
+__device__ __forceinline__ xd dist2d(xd ax, xd ay, xd bx, xd by) {
+  const xd dx = ax - bx, dy = ay - by;  // (a - b).norm()
+  return xsqrt(dx * dx + dy * dy);
+}
+
+// segment_distance(p, a, b), vec2.hpp:48-56.
+__device__ __forceinline__ xd segment_distance(xd px, xd py, xd ax, xd ay, xd bx, xd by) {
+  const xd abx = bx - ax, aby = by - ay;
+  const xd len2 = abx * abx + aby * aby;
+  if (len2.v == 0.0) return dist2d(px, py, ax, ay);
+  xd t = ((px - ax) * abx + (py - ay) * aby) / len2;
+  if (t.v < 0.0) t = 0.0;
+  if (t.v > 1.0) t = 1.0;
+  return dist2d(px, py, ax + abx * t, ay + aby * t);
+}
+
+// ---- detail/arrival_math.hpp:15-69 --------------------------------------
+__device__ __forceinline__ xd rest_to_rest_time(xd L, xd a, xd b, xd vmax) {
+  const xd peak2 = ((xd(2.0) * a) * b * L) / (a + b);
+  const xd peak = xsqrt(peak2);
+  if (peak <= vmax) return peak / a + peak / b;
+  const xd d_used = (vmax * vmax) / (xd(2.0) * a) + (vmax * vmax) / (xd(2.0) * b);
+  return vmax / a + vmax / b + (L - d_used) / vmax;
+}
+
+__device__ __forceinline__ xd one_d_time_to_rest(xd v0, xd dist, xd a, xd b, xd vmax) {
+  const xd brake_dist = (v0 * v0) / (xd(2.0) * b);
+  if (v0.v < 0.0 || brake_dist > dist) {
+    const xd gap = brake_dist - xd(copysign(dist.v, v0.v));
+    return xfabs(v0) / b + rest_to_rest_time(gap, a, b, vmax);
+  }
+  const xd peak2 = ((xd(2.0) * a) * b * dist + b * (v0 * v0)) / (a + b);
+  const xd peak = xsqrt(peak2);
+  if (peak <= vmax) return (peak - v0) / a + peak / b;
+  if (v0 <= vmax) {
+    const xd d_used = (vmax * vmax - v0 * v0) / (xd(2.0) * a) + (vmax * vmax) / (xd(2.0) * b);
+    return (vmax - v0) / a + vmax / b + (dist - d_used) / vmax;
+  }
+  const xd d_used = (v0 * v0 - vmax * vmax) / (xd(2.0) * b) + (vmax * vmax) / (xd(2.0) * b);
+  return (v0 - vmax) / b + vmax / b + (dist - d_used) / vmax;
+}
+
+__device__ __forceinline__ xd arrival_given(xd qx, xd qy, xd d2, xd vx, xd vy, xd a, xd b,
+                                            xd vmax, xd radius) {
+  const xd d = xsqrt(d2);
+  const xd deff_raw = d - radius;
+  const xd deff = deff_raw.v > 0.0 ? deff_raw : xd(0.0);
+  const xd denom = d.v > 1e-30 ? d : xd(1e-30);
+  const xd ex = qx / denom;
+  const xd ey = qy / denom;
+  const xd va = vx * ex + vy * ey;
+  const xd vc = vx * ey - vy * ex;
+  const xd t_along = one_d_time_to_rest(va, deff, a, b, vmax);
+  const xd t_cross = xfabs(vc) / b;
+  return t_along > t_cross ? t_along : t_cross;
+}
+
+__device__ __forceinline__ xd arrival_to_point(xd tx, xd ty, xd px, xd py, xd vx, xd vy, xd a,
+                                               xd b, xd vmax, xd radius) {
+  const xd qx = tx - px;
+  const xd qy = ty - py;
+  return arrival_given(qx, qy, qx * qx + qy * qy, vx, vy, a, b, vmax, radius);
+}
+
+// arrival_time(robot, target, limits), motion.cpp:16-29 (radius 0).
+__device__ __forceinline__ xd arrival_time(xd px, xd py, xd vx, xd vy, xd tx, xd ty, xd a, xd b,
+                                           xd vmax) {
+  const xd qx = tx - px;
+  const xd qy = ty - py;
+  const xd d2 = qx * qx + qy * qy;
+  if (d2.v <= 1e-24) {
+    const xd speed = xsqrt(vx * vx + vy * vy);
+    return one_d_time_to_rest(speed, 0.0, a, b, vmax);
+  }
+  return arrival_given(qx, qy, d2, vx, vy, a, b, vmax, 0.0);
+}
+
+// ---- ball_model.cpp:12-43, 83-107 ---------------------------------------
+struct Traj {
+  xd speed, v1, t_se, d_se, t_stop, d_stop, from;  // from = interceptable_from
+};
+
+__device__ __forceinline__ Traj resolve_kick(xd speed, bool chip, xd slide, xd roll, xd ratio,
+                                             xd chip_frac) {
+  Traj t;
+  t.speed = speed;
+  t.v1 = ratio * speed;
+  t.t_se = (speed - t.v1) / slide;
+  t.d_se = (speed * speed - t.v1 * t.v1) / (xd(2.0) * slide);
+  t.t_stop = t.t_se + t.v1 / roll;
+  t.d_stop = t.d_se + (t.v1 * t.v1) / (xd(2.0) * roll);
+  t.from = chip ? chip_frac * t.d_stop : xd(0.0);
+  return t;
+}
+
+__device__ __forceinline__ xd distance_at(const Traj& tr, xd slide, xd roll, xd t) {
+  if (t < tr.t_se) return tr.speed * t - xd(0.5) * slide * t * t;
+  if (t < tr.t_stop) {
+    const xd u = t - tr.t_se;
+    return tr.d_se + tr.v1 * u - xd(0.5) * roll * u * u;
+  }
+  return tr.d_stop;
+}
+
+// travel_time_to_distance; returns NaN for nullopt (d beyond the rollout).
+__device__ __forceinline__ xd travel_time_to_distance(const Traj& tr, xd slide, xd roll, xd d) {
+  if (d.v == 0.0) return 0.0;
+  if (d > tr.d_stop) return CUDART_NAN;
+  if (d <= tr.d_se) {
+    const xd rad = tr.speed * tr.speed - xd(2.0) * slide * d;
+    return xd(2.0) * d / (tr.speed + xsqrt(rad.v < 0.0 ? xd(0.0) : rad));
+  }
+  const xd rem = d - tr.d_se;
+  const xd rad = tr.v1 * tr.v1 - xd(2.0) * roll * rem;
+  return tr.t_se + xd(2.0) * rem / (tr.v1 + xsqrt(rad.v < 0.0 ? xd(0.0) : rad));
+}
+
+// ray_exit_distance, intercept.cpp:27-43.  Returns NaN when the origin is
+// outside the field (nullopt).
+__device__ __forceinline__ xd ray_exit_distance(xd L, xd W, xd ox, xd oy, xd ux, xd uy) {
+  const xd hx = xd(0.5) * L;
+  const xd hy = xd(0.5) * W;
+  if (!(ox.v >= -hx.v && ox.v <= hx.v && oy.v >= -hy.v && oy.v <= hy.v)) return CUDART_NAN;
+  // std::min(a, b) == (b < a ? b : a); std::max(a, b) == (a < b ? b : a).
+  xd s_exit = CUDART_INF;
+  auto take_min = [&](xd c) { if (c < s_exit) s_exit = c; };
+  if (ux.v > 0.0) {
+    take_min((hx - ox) / ux);
+  } else if (ux.v < 0.0) {
+    take_min((-hx - ox) / ux);
+  }
+  if (uy.v > 0.0) {
+    take_min((hy - oy) / uy);
+  } else if (uy.v < 0.0) {
+    take_min((-hy - oy) / uy);
+  }
+  return s_exit.v < 0.0 ? xd(0.0) : s_exit;
+}
+
+__device__ __forceinline__ xd clamp01(xd x) { return x.v < 0.0 ? xd(0.0) : (x.v > 1.0 ? xd(1.0) : x); }
+
+}  // namespace pp
