@@ -35,21 +35,29 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_product(force: bool = False, verbose_ptxas: bool = False) -> str:
+PROF_LIB = os.path.join(LIB_DIR, "libpassplan_b200_prof.so")
+
+
+def build_product(force: bool = False, verbose_ptxas: bool = False, profile: bool = False) -> str:
+    """profile=True builds lib/libpassplan_b200_prof.so with per-phase cycle
+    counters (-DPP_PHASE_CLOCKS); never used by tests or the bench."""
     os.makedirs(LIB_DIR, exist_ok=True)
+    target = PROF_LIB if profile else LIB
     srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC))
             if f.endswith((".cu", ".cuh", ".h", ".hpp"))]
     hdrs = [os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))
             if f.endswith(".h")]
-    if force or _stale(LIB, srcs + hdrs):
+    if force or _stale(target, srcs + hdrs):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17",
                "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-shared",
-               "-I", os.path.join(ROOT, "include"), "-o", LIB,
+               "-I", os.path.join(ROOT, "include"), "-o", target,
                os.path.join(CSRC, "pp_cabi.cu")]
+        if profile:
+            cmd.insert(1, "-DPP_PHASE_CLOCKS")
         if verbose_ptxas:
             cmd.insert(1, "-Xptxas=-v")
         _run(cmd)
-    return LIB
+    return target
 
 
 def build_checkers() -> None:

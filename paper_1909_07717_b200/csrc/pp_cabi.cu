@@ -371,10 +371,9 @@ cudaError_t ensure_dirs(pp_ctx* ctx, int n) {
   return e;
 }
 
-int warps_for(int n_scan) {
-  int w = n_scan < 4 ? 4 : n_scan;
-  return w > 16 ? 16 : w;
-}
+// CTA width: kCtaWarps warps share the robots of a tile; small CTAs let several
+// co-reside per SM so one CTA's serial phases overlap another's scan.
+int warps_for(int /*n_scan*/) { return pp::kCtaWarps; }
 
 }  // namespace
 
@@ -563,7 +562,7 @@ pp_status pp_score_cells(pp_ctx* ctx, const pp_world* world, const pp_params* pa
   cudaStream_t s = ctx->stream;
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->frame.p, F, sizeof(pp::FrameDev), cudaMemcpyHostToDevice, s));
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->scratch_in.p, in.data(), in.size() * 8, cudaMemcpyHostToDevice, s));
-  const int blocks = static_cast<int>((n + 7) / 8);
+  const int blocks = static_cast<int>((n + 255) / 256);
   pp::score_cells_kernel<<<blocks, 256, 0, s>>>(static_cast<const pp::FrameDev*>(ctx->frame.p), P,
                                                 n, static_cast<const double*>(ctx->scratch_in.p),
                                                 static_cast<double*>(ctx->scratch_out.p));
@@ -605,7 +604,7 @@ pp_status pp_goal_views(pp_ctx* ctx, const pp_world* world, double robot_radius,
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->frame.p, F, sizeof(pp::FrameDev), cudaMemcpyHostToDevice, s));
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->scratch_in.p, in.data(), in.size() * 8, cudaMemcpyHostToDevice, s));
   const double* dpx = static_cast<const double*>(ctx->scratch_in.p);
-  pp::goal_view_kernel<<<static_cast<int>((n + 7) / 8), 256, 0, s>>>(
+  pp::goal_view_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(
       static_cast<const pp::FrameDev*>(ctx->frame.p), robot_radius, n, dpx, dpx + n,
       static_cast<double*>(ctx->scratch_out.p));
   PP_CUDA_TRY(ctx, cudaGetLastError());
@@ -961,3 +960,17 @@ pp_status pp_dpps_batch(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
 }
 
 }  // extern "C"
+
+#ifdef PP_PHASE_CLOCKS
+// Profiling build only: cumulative SM cycles per dpps_kernel phase (A..E) and
+// the number of CTAs that contributed.
+extern "C" int pp_debug_phase_cycles(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, pp::g_phase_cycles, 8 * sizeof(unsigned long long)) != cudaSuccess)
+    return PP_CUDA;
+  if (reset) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(pp::g_phase_cycles, z, sizeof(z)) != cudaSuccess) return PP_CUDA;
+  }
+  return PP_OK;
+}
+#endif
