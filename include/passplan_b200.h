@@ -245,6 +245,12 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
                   const pp_search_grid* grid, int32_t kicker_id, uint32_t copy_flags,
                   void* block);
 
+/* Re-launch the last pp_dpps search on its staged frame, asynchronously on
+ * the context's stream, without host copies (device-resident timing). */
+pp_status pp_dpps_relaunch(pp_ctx* ctx);
+/* The context's cudaStream_t, for callers that time or order work on it. */
+void* pp_ctx_stream(pp_ctx* ctx);
+
 /* Cell count of a grid: kick_type_count * n_directions * n_powers. */
 int64_t pp_grid_cells(const pp_search_grid* grid);
 

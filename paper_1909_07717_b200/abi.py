@@ -241,6 +241,9 @@ def _declare(lib):
     lib.pp_host_free.argtypes = [vp]
     lib.pp_host_free.restype = None
     lib.pp_dpps.argtypes = [vp, _P(World), _P(Params), _P(SearchGrid), _I, C.c_uint32, vp]
+    lib.pp_dpps_relaunch.argtypes = [vp]
+    lib.pp_ctx_stream.argtypes = [vp]
+    lib.pp_ctx_stream.restype = vp
     dp = _P(C.c_double)
     lib.pp_score_cells.argtypes = [vp, _P(World), _P(Params), C.c_int64, dp, dp, dp, dp,
                                    _P(C.c_uint8), dp, _P(PassFeatures)]
@@ -252,7 +255,7 @@ def _declare(lib):
     lib.pp_batch_upload.argtypes = [vp, _P(World), C.c_int64, _P(C.c_int32)]
     lib.pp_batch_run.argtypes = [vp, _P(Params), _P(SearchGrid), _P(C.c_float)]
     lib.pp_batch_download.argtypes = [vp, _P(DppsSummary)]
-    for fn in ("pp_params_validate", "pp_ctx_create", "pp_dpps", "pp_score_cells",
+    for fn in ("pp_params_validate", "pp_ctx_create", "pp_dpps", "pp_dpps_relaunch", "pp_score_cells",
                "pp_goal_views", "pp_runmap_count", "pp_runmap", "pp_dpps_batch",
                "pp_batch_upload", "pp_batch_run", "pp_batch_download"):
         getattr(lib, fn).restype = C.c_int
@@ -277,6 +280,6 @@ EXPORTED_SYMBOLS = (
     "pp_params_default", "pp_params_validate", "pp_grid_bytes", "pp_grid_view_of",
     "pp_runmap_bytes", "pp_runmap_view_of", "pp_runmap_count", "pp_ctx_create",
     "pp_ctx_destroy", "pp_last_error", "pp_kernel_name", "pp_abi_version", "pp_host_alloc",
-    "pp_host_free", "pp_dpps", "pp_grid_cells", "pp_score_cells", "pp_goal_views", "pp_runmap",
+    "pp_host_free", "pp_dpps", "pp_dpps_relaunch", "pp_ctx_stream", "pp_grid_cells", "pp_score_cells", "pp_goal_views", "pp_runmap",
     "pp_dpps_batch", "pp_batch_upload", "pp_batch_run", "pp_batch_download",
 )

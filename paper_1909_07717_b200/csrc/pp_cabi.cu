@@ -81,6 +81,12 @@ struct pp_ctx {
   std::vector<pp::FrameDev> batch_host;
   std::vector<int32_t> batch_kickers, batch_poss;
   int64_t batch_n = 0;
+  // last single-frame launch (pp_dpps_relaunch)
+  bool last_valid = false;
+  pp::DevParams last_P{};
+  pp::CellOut last_co{};
+  pp_dpps_summary* last_dsum = nullptr;
+  int last_threads = 0;
 };
 
 namespace {
@@ -375,11 +381,30 @@ cudaError_t ensure_dirs(pp_ctx* ctx, int n) {
 // co-reside per SM so one CTA's serial phases overlap another's scan.
 int warps_for(int /*n_scan*/) { return pp::kCtaWarps; }
 
+// The fused single-frame launch: one CTA per tile, last-CTA-done summary.
+cudaError_t launch_single(pp_ctx* ctx) {
+  const pp::DevParams& P = ctx->last_P;
+  pp::dpps_kernel<true><<<P.n_tiles, ctx->last_threads, 0, ctx->stream>>>(
+      static_cast<const pp::FrameDev*>(ctx->frame.p), static_cast<const double2*>(ctx->dirs.p), P,
+      P.n_tiles, 1, ctx->last_co, static_cast<pp::Partial*>(ctx->partials.p),
+      static_cast<unsigned*>(ctx->counters.p), ctx->last_dsum);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 extern "C" {
 
 int pp_abi_version(void) { return PP_ABI_VERSION; }
+
+void* pp_ctx_stream(pp_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+pp_status pp_dpps_relaunch(pp_ctx* ctx) {
+  if (!ctx || !ctx->last_valid) return fail(ctx, PP_INTERNAL, "no previous pp_dpps launch");
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  PP_CUDA_TRY(ctx, launch_single(ctx));
+  return PP_OK;
+}
 const char* pp_kernel_name(void) { return "sm100a"; }
 
 void pp_params_default(pp_params* p) {
@@ -511,12 +536,12 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   cudaStream_t s = ctx->stream;
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->frame.p, F, sizeof(pp::FrameDev), cudaMemcpyHostToDevice, s));
   PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, s));
-  const int threads = 32 * warps_for(F->n_scan);
-  pp::dpps_kernel<true><<<P.n_tiles, threads, 0, s>>>(
-      static_cast<const pp::FrameDev*>(ctx->frame.p), static_cast<const double2*>(ctx->dirs.p), P,
-      P.n_tiles, 1, co, static_cast<pp::Partial*>(ctx->partials.p),
-      static_cast<unsigned*>(ctx->counters.p), dsum);
-  PP_CUDA_TRY(ctx, cudaGetLastError());
+  ctx->last_P = P;
+  ctx->last_co = co;
+  ctx->last_dsum = dsum;
+  ctx->last_threads = 32 * warps_for(F->n_scan);
+  ctx->last_valid = true;
+  PP_CUDA_TRY(ctx, launch_single(ctx));
   PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, s));
   const size_t bytes = (copy_flags & PP_COPY_ALL) ? off.total : sizeof(pp_dpps_summary);
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(block, dblk, bytes, cudaMemcpyDeviceToHost, s));
