@@ -23,6 +23,12 @@ _P = C.POINTER
 _dp = _P(C.c_double)
 _vp = C.c_void_p
 
+class OrCounts(C.Structure):
+    """or_counts (oracle/pp_oracle.h): work terms of the reference's pruned scan."""
+    _fields_ = [(n, C.c_uint64) for n in ("quick_rejects", "full_tests", "rest_evals", "scans",
+                                          "bounds")]
+
+
 _ref = None
 _orc = None
 
@@ -86,14 +92,11 @@ def oracle():
                                   C.c_size_t]
         lib.or_direction_table.argtypes = [C.c_int32, _dp]
         lib.or_direction_table.restype = None
-        lib.or_random_world.argtypes = [C.c_uint64, C.c_int32, C.c_int32, W]
-        lib.or_random_world.restype = None
         lib.or_nearest_teammate.argtypes = [W]
         lib.or_nearest_teammate.restype = C.c_int32
-        lib.or_batch.argtypes = [W, C.c_int64, Pm, G, _P(C.c_int32), C.c_int32,
-                                 _P(C.c_int64), _dp, _P(C.c_int64), _dp]
-        lib.or_batch.restype = C.c_int
-        for fn in ("or_dpps", "or_score_cells", "or_goal_views", "or_runmap"):
+        lib.or_dpps_counted.argtypes = [W, Pm, G, C.c_int32, _vp, _P(OrCounts), C.c_char_p,
+                                        C.c_size_t]
+        for fn in ("or_dpps", "or_dpps_counted", "or_score_cells", "or_goal_views", "or_runmap"):
             getattr(lib, fn).restype = C.c_int
         _orc = lib
     return _orc
