@@ -270,6 +270,7 @@ def load_library(path: str = LIB_PATH):
     CPU fallback for the product path."""
     global _LIB
     if _LIB is None:
+        path = os.environ.get("PP_LIB_PATH", path)  # dev override (variant builds)
         if not os.path.exists(path):
             raise RuntimeError(f"{path} missing: run __graft_entry__.build() (no CPU fallback)")
         _LIB = _declare(C.CDLL(path))

@@ -303,8 +303,29 @@ double host_distance(double ax, double ay, double bx, double by) {
   return std::sqrt(dx * dx + dy * dy);
 }
 
+// Smallest double x >= 0 with sqrt_rn(x) >= r, so that for every double x:
+// sqrt_rn(x) < r  <=>  x < sqrt_lt_threshold(r)   (sqrt_rn is monotone).
+double sqrt_lt_threshold(double r) {
+  if (!(r > 0.0)) return 0.0;
+  double x = r * r;
+  while (x > 0.0 && std::sqrt(x) >= r) x = std::nextafter(x, 0.0);
+  while (std::sqrt(x) < r) x = std::nextafter(x, HUGE_VAL);
+  return x;
+}
+
+// Largest double x with sqrt_rn(x) <= m:  sqrt_rn(x) <= m  <=>  x <= result.
+double sqrt_le_threshold(double m) {
+  if (m < 0.0) return -1.0;
+  double x = m * m;
+  while (std::sqrt(x) > m) x = std::nextafter(x, 0.0);
+  while (std::sqrt(std::nextafter(x, HUGE_VAL)) <= m) x = std::nextafter(x, HUGE_VAL);
+  return x;
+}
+
 pp::DevParams make_dev_params(const pp_params& p, const pp_search_grid& g) {
   pp::DevParams d{};
+  d.r_lt2 = sqrt_lt_threshold(p.thresholds.robot_radius);
+  d.mb_le2 = sqrt_le_threshold(p.thresholds.robot_radius + 1e-9);
   d.slide = p.ball.slide_decel;
   d.roll = p.ball.roll_decel;
   d.ratio = p.ball.transition_ratio;
@@ -630,7 +651,8 @@ pp_status pp_goal_views(pp_ctx* ctx, const pp_world* world, double robot_radius,
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->scratch_in.p, in.data(), in.size() * 8, cudaMemcpyHostToDevice, s));
   const double* dpx = static_cast<const double*>(ctx->scratch_in.p);
   pp::goal_view_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(
-      static_cast<const pp::FrameDev*>(ctx->frame.p), robot_radius, n, dpx, dpx + n,
+      static_cast<const pp::FrameDev*>(ctx->frame.p), robot_radius,
+      sqrt_lt_threshold(robot_radius), sqrt_le_threshold(robot_radius + 1e-9), n, dpx, dpx + n,
       static_cast<double*>(ctx->scratch_out.p));
   PP_CUDA_TRY(ctx, cudaGetLastError());
   std::vector<double> o(4 * static_cast<size_t>(n));
@@ -995,6 +1017,21 @@ extern "C" int pp_debug_phase_cycles(unsigned long long* out, int reset) {
   if (reset) {
     const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (cudaMemcpyToSymbol(pp::g_phase_cycles, z, sizeof(z)) != cudaSuccess) return PP_CUDA;
+  }
+  return PP_OK;
+}
+#endif
+
+#ifdef PP_PHASE_CLOCKS
+// Profiling build only: scan counters (iterations, skips, lower-bound
+// rejects, upper-bound accepts, exact FP64 tests, FP64 rounds, sum of per-warp
+// max iterations, robot-warp scans).
+extern "C" int pp_debug_scan_counts(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, pp::g_scan_counts, 16 * sizeof(unsigned long long)) != cudaSuccess)
+    return PP_CUDA;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    if (cudaMemcpyToSymbol(pp::g_scan_counts, z, sizeof(z)) != cudaSuccess) return PP_CUDA;
   }
   return PP_OK;
 }

@@ -22,7 +22,19 @@ cyc = (C.c_uint64 * 8)()
 names = ["A window", "B scan", "C champion", "D value", "E argmax"]
 
 
+lib.pp_debug_scan_counts.argtypes = [C.POINTER(C.c_uint64), C.c_int]
+cnt = (C.c_uint64 * 16)()
+
+
 def report(label):
+    lib.pp_debug_scan_counts(cnt, 1)
+    w = max(cnt[7], 1)
+    lanes = 32 * w
+    print(f"  scans(robot-warps)={cnt[7]} per lane: iters={cnt[0] / lanes:.1f} skips={cnt[1] / lanes:.1f} "
+          f"lb_rej={cnt[2] / lanes:.1f} ub_acc={cnt[3] / lanes:.2f} exact={cnt[4] / lanes:.2f} | "
+          f"per warp: rounds={cnt[5] / w:.2f} max_lane_iters={cnt[6] / w:.1f}")
+    print(f"  cycles per robot-warp scan: setup+prune={cnt[9] / w:.0f} loop={cnt[10] / w:.0f} "
+          f"rest+store={cnt[11] / w:.0f}")
     lib.pp_debug_phase_cycles(cyc, 1)
     n = max(cyc[5], 1)
     tot = sum(cyc[i] for i in range(5))
