@@ -72,6 +72,7 @@ struct pp_ctx {
   std::string err;
   // single frame
   DevBuf frame, block, partials, counters, dirs, scratch_in, scratch_out;
+  DevBuf queue, fcount;  // scan -> value pipeline (per-frame cell queues, counters)
   PinnedBuf frame_h;
   int dirs_n = -1;
   // run map
@@ -400,16 +401,65 @@ cudaError_t ensure_dirs(pp_ctx* ctx, int n) {
 
 // CTA width: kCtaWarps warps share the robots of a tile; small CTAs let several
 // co-reside per SM so one CTA's serial phases overlap another's scan.
-int warps_for(int /*n_scan*/) { return pp::kCtaWarps; }
+int warps_for(int n_scan) {
+  return n_scan < 1 ? 1 : (n_scan > pp::kScanWarps ? pp::kScanWarps : n_scan);
+}
 
-// The fused single-frame launch: one CTA per tile, last-CTA-done summary.
-cudaError_t launch_single(pp_ctx* ctx) {
-  const pp::DevParams& P = ctx->last_P;
-  pp::dpps_kernel<true><<<P.n_tiles, ctx->last_threads, 0, ctx->stream>>>(
-      static_cast<const pp::FrameDev*>(ctx->frame.p), static_cast<const double2*>(ctx->dirs.p), P,
-      P.n_tiles, 1, ctx->last_co, static_cast<pp::Partial*>(ctx->partials.p),
-      static_cast<unsigned*>(ctx->counters.p), ctx->last_dsum);
+int64_t chunks_for(const pp::DevParams& P) {
+  const int64_t n_cells = static_cast<int64_t>(P.n_kt) * P.n_dirs * P.n_pows;
+  return (n_cells + pp::kChunk - 1) / pp::kChunk;
+}
+
+// Queue + counters + partials for `n_frames` frames of this grid shape.
+cudaError_t reserve_pipeline(pp_ctx* ctx, const pp::DevParams& P, int64_t n_frames) {
+  const int64_t n_cells = static_cast<int64_t>(P.n_kt) * P.n_dirs * P.n_pows;
+  const size_t n = static_cast<size_t>(n_frames * n_cells);
+  cudaError_t e = ctx->queue.reserve(n * (4 * sizeof(double) + sizeof(int32_t) + 1) + 64);
+  if (e != cudaSuccess) return e;
+  e = ctx->fcount.reserve(sizeof(pp::FrameCounters) * static_cast<size_t>(n_frames));
+  if (e != cudaSuccess) return e;
+  return ctx->partials.reserve(sizeof(pp::Partial) * static_cast<size_t>(n_frames * chunks_for(P)));
+}
+
+pp::CellQueue make_queue(pp_ctx* ctx, const pp::DevParams& P, int64_t n_frames) {
+  const int64_t n_cells = static_cast<int64_t>(P.n_kt) * P.n_dirs * P.n_pows;
+  const size_t n = static_cast<size_t>(n_frames * n_cells);
+  char* b = static_cast<char*>(ctx->queue.p);
+  pp::CellQueue q;
+  q.rx = reinterpret_cast<double*>(b);
+  q.ry = q.rx + n;
+  q.ot = q.ry + n;
+  q.pt = q.ot + n;
+  q.cell = reinterpret_cast<int32_t*>(q.pt + n);
+  q.slot = reinterpret_cast<int8_t*>(q.cell + n);
+  q.cap = n_cells;
+  return q;
+}
+
+// scan_kernel -> value_kernel for `n_frames` frames (buffers reserved).
+template <bool kCells>
+cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_frames,
+                            const pp::DevParams& P, int scan_threads, const pp::CellOut& co,
+                            pp_dpps_summary* sums) {
+  const pp::CellQueue q = make_queue(ctx, P, n_frames);
+  auto* fc = static_cast<pp::FrameCounters*>(ctx->fcount.p);
+  const int64_t chunks = chunks_for(P);
+  pp::scan_kernel<kCells><<<static_cast<unsigned>(n_frames * P.n_tiles), scan_threads, 0,
+                            ctx->stream>>>(frames, static_cast<const double2*>(ctx->dirs.p), P,
+                                           co, q, fc);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  pp::value_kernel<kCells><<<static_cast<unsigned>(n_frames * chunks), pp::kValueThreads, 0,
+                             ctx->stream>>>(frames, P, q, fc, co,
+                                            static_cast<pp::Partial*>(ctx->partials.p), sums,
+                                            static_cast<int>(chunks));
   return cudaGetLastError();
+}
+
+// The single-frame launch of the last pp_dpps call.
+cudaError_t launch_single(pp_ctx* ctx) {
+  return launch_pipeline<true>(ctx, static_cast<const pp::FrameDev*>(ctx->frame.p), 1,
+                               ctx->last_P, ctx->last_threads, ctx->last_co, ctx->last_dsum);
 }
 
 }  // namespace
@@ -539,8 +589,7 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   const pp::DevParams P = make_dev_params(*params, g);
   PP_CUDA_TRY(ctx, ensure_dirs(ctx, g.n_directions));
   PP_CUDA_TRY(ctx, ctx->block.reserve(off.total));
-  PP_CUDA_TRY(ctx, ctx->partials.reserve(sizeof(pp::Partial) * static_cast<size_t>(P.n_tiles)));
-  PP_CUDA_TRY(ctx, ctx->counters.reserve(sizeof(unsigned) * 4));
+  PP_CUDA_TRY(ctx, reserve_pipeline(ctx, P, 1));
 
   char* dblk = static_cast<char*>(ctx->block.p);
   pp::CellOut co;
@@ -957,16 +1006,18 @@ pp_status pp_batch_run(pp_ctx* ctx, const pp_params* params, const pp_search_gri
   const int threads = 32 * warps_for(max_scan);
   cudaStream_t s = ctx->stream;
   pp::CellOut co{};
+  // Frames are independent: launch them in groups so the per-frame cell
+  // queues stay a bounded working set (group x cells x 37 B).
+  const int64_t n_cells = pp_grid_cells(&g);
+  int64_t group = (int64_t(1) << 28) / std::max<int64_t>(n_cells, 1);
+  group = std::max<int64_t>(1, std::min<int64_t>(group, std::min<int64_t>(n, 4096)));
+  PP_CUDA_TRY(ctx, reserve_pipeline(ctx, P, group));
   PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, s));
-  // Frames are independent: chunk the launch so gridDim.x stays moderate.
-  const int64_t chunk = 1 << 20;
-  for (int64_t f0 = 0; f0 < n; f0 += chunk) {
-    const int64_t nf = std::min(chunk, n - f0);
-    pp::dpps_kernel<false><<<static_cast<unsigned>(nf), threads, 0, s>>>(
-        static_cast<const pp::FrameDev*>(ctx->batch_frames.p) + f0,
-        static_cast<const double2*>(ctx->dirs.p), P, 1, P.n_tiles, co, nullptr, nullptr,
-        static_cast<pp_dpps_summary*>(ctx->batch_sums.p) + f0);
-    PP_CUDA_TRY(ctx, cudaGetLastError());
+  for (int64_t f0 = 0; f0 < n; f0 += group) {
+    const int64_t nf = std::min(group, n - f0);
+    PP_CUDA_TRY(ctx, launch_pipeline<false>(
+                         ctx, static_cast<const pp::FrameDev*>(ctx->batch_frames.p) + f0, nf, P,
+                         threads, co, static_cast<pp_dpps_summary*>(ctx->batch_sums.p) + f0));
   }
   PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, s));
   PP_CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
@@ -1009,13 +1060,13 @@ pp_status pp_dpps_batch(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
 }  // extern "C"
 
 #ifdef PP_PHASE_CLOCKS
-// Profiling build only: cumulative SM cycles per dpps_kernel phase (A..E) and
-// the number of CTAs that contributed.
+// Profiling build only: cumulative SM cycles per phase (scan A/B/C in 0..2,
+// value D1/D2/D3/reduce in 3..6) and CTA counts (scan [8], value [9]).
 extern "C" int pp_debug_phase_cycles(unsigned long long* out, int reset) {
-  if (cudaMemcpyFromSymbol(out, pp::g_phase_cycles, 8 * sizeof(unsigned long long)) != cudaSuccess)
+  if (cudaMemcpyFromSymbol(out, pp::g_phase_cycles, 16 * sizeof(unsigned long long)) != cudaSuccess)
     return PP_CUDA;
   if (reset) {
-    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const unsigned long long z[16] = {0};
     if (cudaMemcpyToSymbol(pp::g_phase_cycles, z, sizeof(z)) != cudaSuccess) return PP_CUDA;
   }
   return PP_OK;

@@ -18,7 +18,7 @@ lib.pp_debug_phase_cycles.argtypes = [C.POINTER(C.c_uint64), C.c_int]
 g = np.load(os.path.join(ROOT, "tests", "golden", "grids.npz"))
 ctx = C.c_void_p()
 assert lib.pp_ctx_create(0, C.byref(ctx)) == 0
-cyc = (C.c_uint64 * 8)()
+cyc = (C.c_uint64 * 16)()
 names = ["A window", "B scan", "C champion", "D value", "E argmax"]
 
 
@@ -36,11 +36,10 @@ def report(label):
     print(f"  cycles per robot-warp scan: setup+prune={cnt[9] / w:.0f} loop={cnt[10] / w:.0f} "
           f"rest+store={cnt[11] / w:.0f}")
     lib.pp_debug_phase_cycles(cyc, 1)
-    n = max(cyc[5], 1)
-    tot = sum(cyc[i] for i in range(5))
-    print(f"{label}: CTAs={cyc[5]} cycles/CTA total={tot / n:.0f} " +
-          " ".join(f"{names[i]}={cyc[i] / n:.0f}({100 * cyc[i] / max(tot, 1):.0f}%)"
-                   for i in range(5)))
+    ns, nv = max(cyc[8], 1), max(cyc[9], 1)
+    print(f"{label}: scan CTAs={cyc[8]} cycles/CTA A={cyc[0] / ns:.0f} B={cyc[1] / ns:.0f} "
+          f"C={cyc[2] / ns:.0f} | value CTAs={cyc[9]} cycles/CTA D1={cyc[3] / nv:.0f} "
+          f"D2={cyc[4] / nv:.0f} D3={cyc[5] / nv:.0f} reduce={cyc[6] / nv:.0f}")
 
 
 w, p, grid, k, _ = case_inputs(g, "f8")
