@@ -399,11 +399,8 @@ cudaError_t ensure_dirs(pp_ctx* ctx, int n) {
   return e;
 }
 
-// CTA width: kCtaWarps warps share the robots of a tile; small CTAs let several
-// co-reside per SM so one CTA's serial phases overlap another's scan.
-int warps_for(int n_scan) {
-  return n_scan < 1 ? 1 : (n_scan > pp::kScanWarps ? pp::kScanWarps : n_scan);
-}
+// Robots scanned per tile (passed on as the scan CTA width request).
+int warps_for(int n_scan) { return n_scan < 1 ? 1 : n_scan; }
 
 int64_t chunks_for(const pp::DevParams& P) {
   const int64_t n_cells = static_cast<int64_t>(P.n_kt) * P.n_dirs * P.n_pows;
@@ -444,9 +441,20 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   const pp::CellQueue q = make_queue(ctx, P, n_frames);
   auto* fc = static_cast<pp::FrameCounters*>(ctx->fcount.p);
   const int64_t chunks = chunks_for(P);
-  pp::scan_kernel<kCells><<<static_cast<unsigned>(n_frames * P.n_tiles), scan_threads, 0,
-                            ctx->stream>>>(frames, static_cast<const double2*>(ctx->dirs.p), P,
-                                           co, q, fc);
+  const int n_scan = scan_threads / 32;
+  const int64_t ctas = n_frames * P.n_tiles;
+  const double2* dirs = static_cast<const double2*>(ctx->dirs.p);
+  // Latency (few tiles): one warp per robot.  Throughput (>= 2 waves of the
+  // narrow shape): 4-warp CTAs, 8 per SM, robots round-robin over the warps.
+  if (ctas >= 2 * 148 * pp::kScanCtasNarrow) {
+    const int w = n_scan < pp::kScanWarpsNarrow ? n_scan : pp::kScanWarpsNarrow;
+    pp::scan_kernel<kCells, pp::kScanWarpsNarrow, pp::kScanCtasNarrow>
+        <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, dirs, P, co, q, fc);
+  } else {
+    const int w = n_scan < pp::kScanWarpsWide ? n_scan : pp::kScanWarpsWide;
+    pp::scan_kernel<kCells, pp::kScanWarpsWide, pp::kScanCtasWide>
+        <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, dirs, P, co, q, fc);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   pp::value_kernel<kCells><<<static_cast<unsigned>(n_frames * chunks), pp::kValueThreads, 0,
