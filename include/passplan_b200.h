@@ -250,6 +250,9 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
 pp_status pp_dpps_relaunch(pp_ctx* ctx);
 /* The context's cudaStream_t, for callers that time or order work on it. */
 void* pp_ctx_stream(pp_ctx* ctx);
+/* Measurement helper: re-run the last pp_dpps search `reps` times with CUDA
+ * events around each of its two kernels (scan, value); average ms of each. */
+pp_status pp_dpps_kernel_times(pp_ctx* ctx, int32_t reps, float* scan_ms, float* value_ms);
 
 /* Cell count of a grid: kick_type_count * n_directions * n_powers. */
 int64_t pp_grid_cells(const pp_search_grid* grid);

@@ -242,6 +242,8 @@ def _declare(lib):
     lib.pp_host_free.restype = None
     lib.pp_dpps.argtypes = [vp, _P(World), _P(Params), _P(SearchGrid), _I, C.c_uint32, vp]
     lib.pp_dpps_relaunch.argtypes = [vp]
+    lib.pp_dpps_kernel_times.argtypes = [vp, _I, _P(C.c_float), _P(C.c_float)]
+    lib.pp_dpps_kernel_times.restype = C.c_int
     lib.pp_ctx_stream.argtypes = [vp]
     lib.pp_ctx_stream.restype = vp
     dp = _P(C.c_double)
@@ -281,6 +283,7 @@ EXPORTED_SYMBOLS = (
     "pp_params_default", "pp_params_validate", "pp_grid_bytes", "pp_grid_view_of",
     "pp_runmap_bytes", "pp_runmap_view_of", "pp_runmap_count", "pp_ctx_create",
     "pp_ctx_destroy", "pp_last_error", "pp_kernel_name", "pp_abi_version", "pp_host_alloc",
-    "pp_host_free", "pp_dpps", "pp_dpps_relaunch", "pp_ctx_stream", "pp_grid_cells", "pp_score_cells", "pp_goal_views", "pp_runmap",
+    "pp_host_free", "pp_dpps", "pp_dpps_relaunch", "pp_ctx_stream", "pp_dpps_kernel_times",
+    "pp_grid_cells", "pp_score_cells", "pp_goal_views", "pp_runmap",
     "pp_dpps_batch", "pp_batch_upload", "pp_batch_run", "pp_batch_download",
 )

@@ -68,7 +68,7 @@ struct PinnedBuf {
 struct pp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evm = nullptr;
   std::string err;
   // single frame
   DevBuf frame, block, partials, counters, dirs, scratch_in, scratch_out;
@@ -437,7 +437,7 @@ pp::CellQueue make_queue(pp_ctx* ctx, const pp::DevParams& P, int64_t n_frames) 
 template <bool kCells>
 cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_frames,
                             const pp::DevParams& P, int scan_threads, const pp::CellOut& co,
-                            pp_dpps_summary* sums) {
+                            pp_dpps_summary* sums, cudaEvent_t mid = nullptr) {
   const pp::CellQueue q = make_queue(ctx, P, n_frames);
   auto* fc = static_cast<pp::FrameCounters*>(ctx->fcount.p);
   const int64_t chunks = chunks_for(P);
@@ -457,6 +457,7 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (mid) cudaEventRecord(mid, ctx->stream);
   pp::value_kernel<kCells><<<static_cast<unsigned>(n_frames * chunks), pp::kValueThreads, 0,
                              ctx->stream>>>(frames, P, q, fc, co,
                                             static_cast<pp::Partial*>(ctx->partials.p), sums,
@@ -465,9 +466,9 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
 }
 
 // The single-frame launch of the last pp_dpps call.
-cudaError_t launch_single(pp_ctx* ctx) {
+cudaError_t launch_single(pp_ctx* ctx, cudaEvent_t mid = nullptr) {
   return launch_pipeline<true>(ctx, static_cast<const pp::FrameDev*>(ctx->frame.p), 1,
-                               ctx->last_P, ctx->last_threads, ctx->last_co, ctx->last_dsum);
+                               ctx->last_P, ctx->last_threads, ctx->last_co, ctx->last_dsum, mid);
 }
 
 }  // namespace
@@ -482,6 +483,26 @@ pp_status pp_dpps_relaunch(pp_ctx* ctx) {
   if (!ctx || !ctx->last_valid) return fail(ctx, PP_INTERNAL, "no previous pp_dpps launch");
   PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   PP_CUDA_TRY(ctx, launch_single(ctx));
+  return PP_OK;
+}
+
+pp_status pp_dpps_kernel_times(pp_ctx* ctx, int32_t reps, float* scan_ms, float* value_ms) {
+  if (!ctx || !ctx->last_valid || reps < 1) return fail(ctx, PP_INTERNAL, "no previous pp_dpps launch");
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  double a = 0.0, b = 0.0;
+  for (int i = 0; i < reps; ++i) {
+    PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    PP_CUDA_TRY(ctx, launch_single(ctx, ctx->evm));
+    PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+    PP_CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
+    float x = 0.f, y = 0.f;
+    cudaEventElapsedTime(&x, ctx->ev0, ctx->evm);
+    cudaEventElapsedTime(&y, ctx->evm, ctx->ev1);
+    a += x;
+    b += y;
+  }
+  if (scan_ms) *scan_ms = static_cast<float>(a / reps);
+  if (value_ms) *value_ms = static_cast<float>(b / reps);
   return PP_OK;
 }
 const char* pp_kernel_name(void) { return "sm100a"; }
@@ -548,7 +569,8 @@ pp_status pp_ctx_create(int device, pp_ctx** out) {
   if (cudaSetDevice(device) != cudaSuccess) return PP_CUDA;
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
     return PP_CUDA;
-  if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess)
+  if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
+      cudaEventCreate(&ctx->evm) != cudaSuccess)
     return PP_CUDA;
   if (ctx->frame.reserve(sizeof(pp::FrameDev)) != cudaSuccess) return PP_CUDA;
   if (ctx->frame_h.reserve(sizeof(pp::FrameDev)) != cudaSuccess) return PP_CUDA;
@@ -562,6 +584,7 @@ void pp_ctx_destroy(pp_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->evm) cudaEventDestroy(ctx->evm);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

@@ -26,9 +26,13 @@ def run(args):
     return subprocess.run(args, capture_output=True, text=True, check=True).stdout
 
 
-def main(rep, name):
+def main(rep, name, kernel=None):
     raw = list(csv.reader(io.StringIO(run(["ncu", "-i", rep, "--page", "raw", "--csv"]))))
-    hdr, unit, val = raw[0], raw[1], raw[2]
+    hdr, unit = raw[0], raw[1]
+    rows = raw[2:]
+    if kernel:
+        rows = [r for r in rows if kernel in r[hdr.index("Kernel Name")]]
+    val = rows[0]
     out = {"report": os.path.basename(rep), "kernel": val[hdr.index("Kernel Name")][:120]}
     for k in KEYS:
         if k in hdr:
@@ -45,7 +49,10 @@ def main(rep, name):
     dur = out.get("gpu__time_duration.sum")
     if dur:
         out["duration_us"] = dur["value"] * SCALE.get(dur["unit"], 1)
-    src = run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"])
+    src_cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+    if kernel:
+        src_cmd += ["--kernel-name", f"regex:{kernel}"]
+    src = run(src_cmd)
     rows = list(csv.reader(io.StringIO(src)))
     lines, hdr2 = [], None
     for r in rows:
@@ -68,4 +75,4 @@ def main(rep, name):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
