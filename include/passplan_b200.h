@@ -274,6 +274,14 @@ pp_status pp_goal_views(pp_ctx* ctx, const pp_world* world, double robot_radius,
 pp_status pp_runmap(pp_ctx* ctx, const pp_world* world, const pp_params* params,
                     const pp_runmap_request* req, void* block, int64_t block_vertices);
 
+/* score_running_point at n explicit points (offball.cpp:176-201).  ok[i] = 0
+ * where the reference throws domain_error (outside the front field or
+ * strictly inside their defense area); score/features are then undefined. */
+pp_status pp_score_running_points(pp_ctx* ctx, const pp_world* world, const pp_params* params,
+                                  int64_t n, const double* px, const double* py,
+                                  double* score_out, pp_run_features* features_out,
+                                  uint8_t* ok_out);
+
 /* ---- batched frames (log replay / what-if states) ----------------------
  * Independent frames share params and grid; each gets the pp_dpps summary.
  * kicker_ids may be NULL: then the kicker is the teammate nearest the ball

@@ -252,6 +252,9 @@ def _declare(lib):
     lib.pp_goal_views.argtypes = [vp, _P(World), C.c_double, C.c_int64, dp, dp, dp, dp, dp, dp]
     lib.pp_runmap_count.argtypes = [_P(World), _P(Params), C.c_uint32, _P(C.c_int64)]
     lib.pp_runmap.argtypes = [vp, _P(World), _P(Params), _P(RunmapRequest), vp, C.c_int64]
+    lib.pp_score_running_points.argtypes = [vp, _P(World), _P(Params), C.c_int64, dp, dp, dp,
+                                            _P(RunFeatures), _P(C.c_uint8)]
+    lib.pp_score_running_points.restype = C.c_int
     lib.pp_dpps_batch.argtypes = [vp, _P(World), C.c_int64, _P(Params), _P(SearchGrid),
                                   _P(C.c_int32), _P(DppsSummary)]
     lib.pp_batch_upload.argtypes = [vp, _P(World), C.c_int64, _P(C.c_int32)]
@@ -286,4 +289,5 @@ EXPORTED_SYMBOLS = (
     "pp_host_free", "pp_dpps", "pp_dpps_relaunch", "pp_ctx_stream", "pp_dpps_kernel_times",
     "pp_grid_cells", "pp_score_cells", "pp_goal_views", "pp_runmap",
     "pp_dpps_batch", "pp_batch_upload", "pp_batch_run", "pp_batch_download",
+    "pp_score_running_points",
 )

@@ -60,6 +60,37 @@ def build_product(force: bool = False, verbose_ptxas: bool = False, profile: boo
     return target
 
 
+def build_dropin(force: bool = False) -> str:
+    """lib/libpassplan.so: the reference's C++ API (include/passplan/) over the C-ABI."""
+    src = os.path.join(CSRC, "passplan_dropin.cpp")
+    hdrs = [os.path.join(ROOT, "include", "passplan", f)
+            for f in os.listdir(os.path.join(ROOT, "include", "passplan"))]
+    if force or _stale(DROPIN_LIB, [src, LIB] + hdrs):
+        cxx = shutil.which("g++") or "g++"
+        _run([cxx, "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-shared",
+              "-I", os.path.join(ROOT, "include"), "-o", DROPIN_LIB, src,
+              "-L", LIB_DIR, "-lpassplan_b200", "-Wl,-rpath,$ORIGIN"])
+    return DROPIN_LIB
+
+
+CPP_TEST = os.path.join(ROOT, "tests", "cpp", "build", "test_dropin")
+
+
+def build_cpp_tests(force: bool = False) -> str:
+    """tests/cpp/build/test_dropin: C++ parity tests of the drop-in (+ C oracle)."""
+    src = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+    orc = os.path.join(ROOT, "oracle", "pp_oracle.c")
+    os.makedirs(os.path.dirname(CPP_TEST), exist_ok=True)
+    if force or _stale(CPP_TEST, [src, orc, DROPIN_LIB]):
+        obj = CPP_TEST + "_oracle.o"
+        _run([shutil.which("gcc") or "gcc", "-std=c11", "-O2", "-ffp-contract=off", "-c",
+              "-I", os.path.join(ROOT, "include"), orc, "-o", obj])
+        _run([shutil.which("g++") or "g++", "-std=c++20", "-O2", "-ffp-contract=off",
+              "-I", os.path.join(ROOT, "include"), src, obj, "-o", CPP_TEST,
+              "-L", LIB_DIR, "-lpassplan", "-lpassplan_b200", f"-Wl,-rpath,{LIB_DIR}", "-lm"])
+    return CPP_TEST
+
+
 def build_checkers() -> None:
     """oracle/liboracle.so always; oracle/_ref/ when the reference tree exists
     (this container).  The GPU box only uses the prebuilt files."""
@@ -72,7 +103,9 @@ def build_checkers() -> None:
 
 def build_all(force: bool = False) -> None:
     build_product(force=force)
+    build_dropin(force=force)
     build_checkers()
+    build_cpp_tests(force=force)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,569 @@
+// passplan_dropin.cpp -- the reference's C++ API (include/passplan/passplan.hpp)
+// implemented on the C-ABI of passplan_b200.h.  Built into lib/libpassplan.so.
+//
+// Hot-path calls (run_dpps, score_pass, best_pass, goal_view,
+// score_running_point, best_running_points) go to the GPU; the rest are the
+// reference's small closed forms on the host.  Compiled with
+// -ffp-contract=off so the host-side arithmetic rounds like the reference.
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "passplan/passplan.hpp"
+#include "passplan_b200.h"
+
+namespace passplan {
+
+namespace {
+
+// One C-ABI context per host thread (the reference's functions are
+// re-entrant; a pp_ctx is single-threaded).
+struct ThreadCtx {
+  pp_ctx* ctx = nullptr;
+  void* block = nullptr;
+  size_t block_bytes = 0;
+  ~ThreadCtx() {
+    if (block) pp_host_free(block);
+    if (ctx) pp_ctx_destroy(ctx);
+  }
+};
+
+thread_local ThreadCtx tl;
+
+pp_ctx* context() {
+  if (!tl.ctx) {
+    const char* dev = std::getenv("PASSPLAN_DEVICE");
+    const int device = dev ? std::atoi(dev) : 0;
+    if (pp_ctx_create(device, &tl.ctx) != PP_OK || !tl.ctx) {
+      tl.ctx = nullptr;
+      throw internal_error("passplan: no usable CUDA device " + std::to_string(device) +
+                           " (the sm_100a path has no CPU fallback)");
+    }
+  }
+  return tl.ctx;
+}
+
+void* host_block(size_t bytes) {
+  if (bytes > tl.block_bytes) {
+    if (tl.block) pp_host_free(tl.block);
+    tl.block = pp_host_alloc(bytes);
+    if (!tl.block) throw internal_error("passplan: pinned host allocation failed");
+    tl.block_bytes = bytes;
+  }
+  return tl.block;
+}
+
+ErrorCategory category_of(pp_status st) {
+  switch (st) {
+    case PP_SCHEMA: return ErrorCategory::schema;
+    case PP_VALIDATION: return ErrorCategory::validation;
+    case PP_CONFIG: return ErrorCategory::config;
+    case PP_DOMAIN: return ErrorCategory::domain;
+    default: return ErrorCategory::internal;
+  }
+}
+
+void check(pp_status st, pp_ctx* ctx) {
+  if (st != PP_OK) throw Error(category_of(st), ctx ? pp_last_error(ctx) : "passplan error");
+}
+
+pp_robot to_pp(const RobotState& r) {
+  pp_robot o{};
+  o.id = r.id;
+  o.px = r.position.x;
+  o.py = r.position.y;
+  o.vx = r.velocity.x;
+  o.vy = r.velocity.y;
+  o.theta = r.theta;
+  return o;
+}
+
+pp_world to_pp(const WorldState& w) {
+  if (w.ours.size() > PP_MAX_TEAM || w.theirs.size() > PP_MAX_TEAM)
+    throw validation_error("more than 16 robots on a team");
+  pp_world o;
+  std::memset(&o, 0, sizeof(o));
+  o.field = {w.field.length, w.field.width, w.field.goal_width, w.field.defense_depth,
+             w.field.defense_width};
+  o.ball_px = w.ball.position.x;
+  o.ball_py = w.ball.position.y;
+  o.ball_vx = w.ball.velocity.x;
+  o.ball_vy = w.ball.velocity.y;
+  o.n_ours = static_cast<int32_t>(w.ours.size());
+  o.n_theirs = static_cast<int32_t>(w.theirs.size());
+  for (size_t i = 0; i < w.ours.size(); ++i) o.ours[i] = to_pp(w.ours[i]);
+  for (size_t i = 0; i < w.theirs.size(); ++i) o.theirs[i] = to_pp(w.theirs[i]);
+  return o;
+}
+
+pp_search_grid to_pp(const SearchGrid& g) {
+  return {g.n_directions, g.n_powers, g.power_min, g.power_max, g.flat ? 1 : 0, g.chip ? 1 : 0};
+}
+
+pp_params to_pp(const PlannerConfig& c) {
+  pp_params p;
+  std::memset(&p, 0, sizeof(p));
+  p.ball = {c.ball.slide_decel, c.ball.roll_decel, c.ball.transition_ratio, c.ball.power_min,
+            c.ball.power_max, c.ball.chip_flight_fraction};
+  p.motion_ours = {c.motion_ours.max_speed, c.motion_ours.max_accel, c.motion_ours.max_decel};
+  p.motion_theirs = {c.motion_theirs.max_speed, c.motion_theirs.max_accel,
+                     c.motion_theirs.max_decel};
+  p.grid = to_pp(c.grid);
+  const PassWeights& pw = c.weights.pass;
+  p.pass_weights = {pw.teammate_time, pw.shoot_angle, pw.dist_goal, pw.refraction, pw.margin};
+  const RunWeights& rw = c.weights.run;
+  p.run_weights = {rw.dist_goal, rw.dist_ball, rw.angle, rw.guard_time, rw.exposure};
+  p.norm = {c.weights.norm.length_upper, c.weights.norm.angle_upper};
+  p.angle_band = {c.angle_band.full_lo, c.angle_band.peak_lo, c.angle_band.peak_hi,
+                  c.angle_band.full_hi};
+  const PlannerThresholds& t = c.thresholds;
+  p.thresholds = {t.sbip_dt,         t.robot_radius,    t.safety_margin,  t.buffer_time,
+                  t.possession_radius, t.angle_threshold, t.shot_power,   t.margin_cap,
+                  t.possession_dt,   t.contest_epsilon, t.grid_step,      t.min_zone_width,
+                  t.guard_time_cap,  t.drag_v_min,      t.marking_radius};
+  return p;
+}
+
+PassFeatures from_pp(const pp_pass_features& f) {
+  return {f.teammate_intercept_time, f.shoot_angle_at_receive, f.dist_receive_to_goal,
+          f.refraction_angle, f.intercept_margin};
+}
+
+RunningPointFeatures from_pp(const pp_run_features& f) {
+  return {f.dist_to_goal, f.dist_to_ball, f.angle_to_goal, f.guard_time, f.defense_exposure};
+}
+
+int axis_count(double span, double step) {  // offball.cpp:69-74
+  const int n = static_cast<int>(std::floor(span / step + 1e-9)) + 1;
+  return n > 0 ? n : 0;
+}
+
+std::vector<double> axis_lattice(double anchor, double span, double direction, double step) {
+  const int n = axis_count(span, step);
+  std::vector<double> v(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) v[static_cast<size_t>(i)] = anchor + direction * (i * step);
+  return v;
+}
+
+}  // namespace
+
+// ---- host closed forms -------------------------------------------------------
+
+double segment_distance(Vec2 p, Vec2 a, Vec2 b) {
+  const Vec2 ab = b - a;
+  const double len2 = ab.norm2();
+  if (len2 == 0.0) return distance(p, a);
+  double t = (p - a).dot(ab) / len2;
+  t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+  return distance(p, a + ab * t);
+}
+
+const char* category_name(ErrorCategory c) {
+  switch (c) {
+    case ErrorCategory::schema: return "schema";
+    case ErrorCategory::validation: return "validation";
+    case ErrorCategory::config: return "config";
+    case ErrorCategory::domain: return "domain";
+    case ErrorCategory::internal: return "internal";
+  }
+  return "internal";
+}
+
+int exit_code_for(ErrorCategory c) {
+  switch (c) {
+    case ErrorCategory::schema:
+    case ErrorCategory::validation: return 2;
+    case ErrorCategory::config: return 3;
+    default: return 4;
+  }
+}
+
+void FieldGeometry::validate() const {
+  if (!(length > 0.0) || !(width > 0.0)) throw config_error("field dimensions must be positive");
+  if (!(goal_width > 0.0) || goal_width > width) throw config_error("goal_width out of range");
+  if (!(defense_depth > 0.0) || defense_depth > length)
+    throw config_error("defense_depth out of range");
+  if (!(defense_width > 0.0) || defense_width > width)
+    throw config_error("defense_width out of range");
+}
+
+const RobotState* WorldState::find(Team t, int id) const {
+  for (const RobotState& r : team(t))
+    if (r.id == id) return &r;
+  return nullptr;
+}
+
+void WorldState::validate() const {
+  field.validate();
+  const double hx = 0.5 * field.length + 0.5, hy = 0.5 * field.width + 0.5;
+  auto inside = [&](Vec2 p) { return p.x >= -hx && p.x <= hx && p.y >= -hy && p.y <= hy; };
+  if (!inside(ball.position)) throw validation_error("ball outside field bounds");
+  for (const auto* team : {&ours, &theirs}) {
+    const char* name = team == &ours ? "ours" : "theirs";
+    if (team->size() > 16)
+      throw validation_error(std::string(name) + ": more than 16 robots");
+    std::set<int> ids;
+    for (const RobotState& r : *team) {
+      if (!ids.insert(r.id).second)
+        throw validation_error(std::string(name) + ": duplicate robot id " + std::to_string(r.id));
+      if (!inside(r.position))
+        throw validation_error(std::string(name) + ": robot " + std::to_string(r.id) +
+                               " outside field bounds");
+      if (!(r.velocity.norm() <= 5.0))
+        throw validation_error(std::string(name) + ": robot " + std::to_string(r.id) +
+                               " faster than 5 m/s");
+    }
+  }
+}
+
+WorldState mirror_world(const WorldState& w) {
+  WorldState m = w;
+  m.ball.position.y = -m.ball.position.y;
+  m.ball.velocity.y = -m.ball.velocity.y;
+  for (auto* team : {&m.ours, &m.theirs}) {
+    for (RobotState& r : *team) {
+      r.position.y = -r.position.y;
+      r.velocity.y = -r.velocity.y;
+      r.theta = -r.theta;
+    }
+  }
+  return m;
+}
+
+void BallModelParams::validate() const {
+  pp_params p;
+  pp_params_default(&p);
+  p.ball = {slide_decel, roll_decel, transition_ratio, power_min, power_max, chip_flight_fraction};
+  char msg[256];
+  if (pp_params_validate(&p, msg, sizeof(msg)) != PP_OK) throw config_error(msg);
+}
+
+void MotionLimits::validate() const {
+  if (!(max_speed > 0.0) || !(max_accel > 0.0) || !(max_decel > 0.0))
+    throw config_error("motion limits must all be positive");
+}
+
+std::vector<KickType> SearchGrid::kick_types() const {
+  std::vector<KickType> out;
+  if (flat) out.push_back(KickType::flat);
+  if (chip) out.push_back(KickType::chip);
+  return out;
+}
+
+void SearchGrid::validate() const {
+  if (n_directions < 1) throw config_error("grid.n_directions must be >= 1");
+  if (n_powers < 1) throw config_error("grid.n_powers must be >= 1");
+  if (!(power_min > 0.0) || !(power_min <= power_max))
+    throw config_error("grid requires 0 < power_min <= power_max");
+}
+
+void PlannerConfig::validate() const {
+  const pp_params p = to_pp(*this);
+  char msg[256];
+  if (pp_params_validate(&p, msg, sizeof(msg)) != PP_OK) throw config_error(msg);
+}
+
+std::vector<Vec2> direction_table(int n) {
+  std::vector<Vec2> dirs(static_cast<size_t>(n));
+  for (int k = 0; k <= n / 2; ++k) {
+    const double theta = direction_angle(k, n);
+    double c = std::cos(theta), s = std::sin(theta);
+    if (k == 0) {
+      c = -1.0;
+      s = 0.0;
+    }
+    dirs[k] = {c, s};
+    const int m = (n - k) % n;
+    if (m != k) dirs[m] = {c, -s};
+  }
+  return dirs;
+}
+
+std::vector<double> power_table(int n, double power_min, double power_max) {
+  std::vector<double> p(static_cast<size_t>(n));
+  if (n == 1) {
+    p[0] = power_min;
+    return p;
+  }
+  const double span = power_max - power_min;
+  for (int j = 0; j < n; ++j) p[j] = power_min + (j * span) / (n - 1);
+  return p;
+}
+
+std::vector<PassCandidate> feasible_candidates(const CandidateGrid& g) {
+  std::vector<PassCandidate> out;
+  for (const PassCandidate& c : g.cells)
+    if (c.feasible) out.push_back(c);
+  return out;
+}
+
+bool grids_identical(const CandidateGrid& a, const CandidateGrid& b) {
+  if (a.cells.size() != b.cells.size()) return false;
+  for (size_t i = 0; i < a.cells.size(); ++i) {
+    const PassCandidate& x = a.cells[i];
+    const PassCandidate& y = b.cells[i];
+    if (x.kick_type != y.kick_type || x.dir_index != y.dir_index ||
+        x.power_index != y.power_index || x.our_id != y.our_id || x.opp_id != y.opp_id ||
+        x.feasible != y.feasible || x.our_time != y.our_time || x.opp_time != y.opp_time ||
+        x.receive_point.x != y.receive_point.x || x.receive_point.y != y.receive_point.y)
+      return false;
+  }
+  return true;
+}
+
+// ---- GPU path ------------------------------------------------------------------
+
+CandidateGrid run_dpps(const WorldState& world, int kicker_id, const SearchGrid& grid,
+                       const PlannerConfig& cfg, int workers) {
+  grid.validate();
+  cfg.validate();
+  if (world.find(Team::ours, kicker_id) == nullptr)
+    throw validation_error("kicker id " + std::to_string(kicker_id) + " is not on team ours");
+  pp_ctx* ctx = context();
+  const pp_world w = to_pp(world);
+  const pp_params p = to_pp(cfg);
+  const pp_search_grid g = to_pp(grid);
+  const int64_t n = pp_grid_cells(&g);
+  void* block = host_block(pp_grid_bytes(n));
+  const auto t0 = std::chrono::steady_clock::now();
+  check(pp_dpps(ctx, &w, &p, &g, kicker_id, PP_COPY_ALL, block), ctx);
+  const auto t1 = std::chrono::steady_clock::now();
+  pp_grid_view v;
+  pp_grid_view_of(block, n, &v);
+  const pp_dpps_summary& s = *v.summary;
+
+  CandidateGrid out;
+  out.grid = grid;
+  out.kicker_id = kicker_id;
+  out.ball_origin = world.ball.position;
+  out.kick_types = grid.kick_types();
+  out.directions = direction_table(grid.n_directions);
+  out.powers = power_table(grid.n_powers, grid.power_min, grid.power_max);
+  out.cells.resize(static_cast<size_t>(n));
+  const int nd = grid.n_directions, np = grid.n_powers;
+  for (int64_t i = 0; i < n; ++i) {
+    PassCandidate& c = out.cells[static_cast<size_t>(i)];
+    c.kick_type = out.kick_types[static_cast<size_t>(i / (int64_t(nd) * np))];
+    c.dir_index = static_cast<int>((i / np) % nd);
+    c.power_index = static_cast<int>(i % np);
+    c.our_id = v.our_slot[i] >= 0 ? s.ours_ids[v.our_slot[i]] : -1;
+    c.opp_id = v.opp_slot[i] >= 0 ? s.theirs_ids[v.opp_slot[i]] : -1;
+    c.our_time = v.our_time[i];
+    c.opp_time = v.opp_time[i];
+    if (c.our_time < kNever) c.receive_point = {v.rx[i], v.ry[i]};
+    c.feasible = v.feasible[i] != 0;
+  }
+  out.telemetry.sbip_calls = s.sbip_calls;
+  out.telemetry.wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  out.telemetry.workers = workers < 1 ? 1 : workers;
+  out.telemetry.kernel = pp_kernel_name();
+  out.telemetry.kicker_in_possession = s.kicker_in_possession != 0;
+  return out;
+}
+
+CandidateGrid run_dpps_serial(const WorldState& world, int kicker_id, const SearchGrid& grid,
+                              const PlannerConfig& cfg) {
+  return run_dpps(world, kicker_id, grid, cfg, 1);
+}
+
+GoalView goal_view(Vec2 point, const WorldState& world, double robot_radius) {
+  pp_ctx* ctx = context();
+  const pp_world w = to_pp(world);
+  double a, lo, hi, ty;
+  check(pp_goal_views(ctx, &w, robot_radius, 1, &point.x, &point.y, &a, &lo, &hi, &ty), ctx);
+  GoalView v;
+  v.angle = a;
+  v.window_lo = lo;
+  v.window_hi = hi;
+  v.target = {0.5 * world.field.length, ty};
+  return v;
+}
+
+double shoot_angle(Vec2 point, const WorldState& world, double robot_radius) {
+  return goal_view(point, world, robot_radius).angle;
+}
+
+std::pair<double, PassFeatures> score_pass(const PassCandidate& candidate, const WorldState& world,
+                                           const PlannerConfig& cfg) {
+  if (!candidate.feasible) throw domain_error("score_pass: candidate is not feasible");
+  pp_ctx* ctx = context();
+  const pp_world w = to_pp(world);
+  const pp_params p = to_pp(cfg);
+  const uint8_t feas = 1;
+  double score;
+  pp_pass_features f;
+  check(pp_score_cells(ctx, &w, &p, 1, &candidate.receive_point.x, &candidate.receive_point.y,
+                       &candidate.our_time, &candidate.opp_time, &feas, &score, &f),
+        ctx);
+  return {score, from_pp(f)};
+}
+
+std::optional<ScoredPass> best_pass(const CandidateGrid& g, const WorldState& world,
+                                    const PlannerConfig& cfg, std::optional<KickType> only) {
+  std::vector<size_t> idx;
+  for (size_t i = 0; i < g.cells.size(); ++i) {
+    const PassCandidate& c = g.cells[i];
+    if (c.feasible && (!only || c.kick_type == *only)) idx.push_back(i);
+  }
+  if (idx.empty()) return std::nullopt;
+  const size_t n = idx.size();
+  std::vector<double> rx(n), ry(n), ot(n), pt(n), score(n);
+  std::vector<uint8_t> feas(n, 1);
+  std::vector<pp_pass_features> feat(n);
+  for (size_t k = 0; k < n; ++k) {
+    const PassCandidate& c = g.cells[idx[k]];
+    rx[k] = c.receive_point.x;
+    ry[k] = c.receive_point.y;
+    ot[k] = c.our_time;
+    pt[k] = c.opp_time;
+  }
+  pp_ctx* ctx = context();
+  const pp_world w = to_pp(world);
+  const pp_params p = to_pp(cfg);
+  check(pp_score_cells(ctx, &w, &p, static_cast<int64_t>(n), rx.data(), ry.data(), ot.data(),
+                       pt.data(), feas.data(), score.data(), feat.data()),
+        ctx);
+  size_t best = 0;  // first strict max in cell order (pass_eval.cpp:178-185)
+  for (size_t k = 1; k < n; ++k)
+    if (score[k] > score[best]) best = k;
+  return ScoredPass{g.cells[idx[best]], score[best], from_pp(feat[best])};
+}
+
+std::optional<ScoredPass> best_pass(const CandidateGrid& g, const WorldState& world,
+                                    const PlannerConfig& cfg) {
+  return best_pass(g, world, cfg, std::nullopt);
+}
+
+// ---- running points ----------------------------------------------------------
+
+const char* zone_name(ZoneLabel z) {
+  switch (z) {
+    case ZoneLabel::I: return "I";
+    case ZoneLabel::II: return "II";
+    case ZoneLabel::III: return "III";
+    default: return "IV";
+  }
+}
+
+std::optional<ZoneLabel> ZonePartition::label_at(Vec2 p) const {
+  if (p.x < zones[0].x0 || p.x > zones[2].x1 || p.y < zones[1].y0 || p.y > zones[0].y1)
+    return std::nullopt;
+  if (p.x >= cut_x) return p.y >= cut_y ? ZoneLabel::III : ZoneLabel::IV;
+  return p.y >= cut_y ? ZoneLabel::I : ZoneLabel::II;
+}
+
+ZonePartition partition_zones(const FieldGeometry& field, Vec2 ball, double min_zone_width) {
+  if (!(min_zone_width > 0.0) || 2.0 * min_zone_width > field.width)
+    throw config_error("min_zone_width must be positive and at most half the field width");
+  ZonePartition part;
+  part.cut_x = 0.25 * field.length;
+  part.cut_y = std::clamp(ball.y, -0.5 * field.width + min_zone_width,
+                          0.5 * field.width - min_zone_width);
+  const double x_mid = 0.5 * field.length, y_top = 0.5 * field.width;
+  part.zones[0] = {ZoneLabel::I, 0.0, part.cut_x, part.cut_y, y_top};
+  part.zones[1] = {ZoneLabel::II, 0.0, part.cut_x, -y_top, part.cut_y};
+  part.zones[2] = {ZoneLabel::III, part.cut_x, x_mid, part.cut_y, y_top};
+  part.zones[3] = {ZoneLabel::IV, part.cut_x, x_mid, -y_top, part.cut_y};
+  return part;
+}
+
+std::vector<Vec2> zone_lattice(const Zone& zone, double step) {
+  if (!(step > 0.0)) throw config_error("lattice step must be positive");
+  const bool upper = zone.label == ZoneLabel::I || zone.label == ZoneLabel::III;
+  const auto xs = axis_lattice(zone.x0, zone.x1 - zone.x0, 1.0, step);
+  const auto ys = upper ? axis_lattice(zone.y0, zone.y1 - zone.y0, 1.0, step)
+                        : axis_lattice(zone.y1, zone.y1 - zone.y0, -1.0, step);
+  std::vector<Vec2> out;
+  out.reserve(xs.size() * ys.size());
+  for (double x : xs)
+    for (double y : ys) out.push_back({x, y});
+  return out;
+}
+
+std::pair<double, RunningPointFeatures> score_running_point(Vec2 pt, const WorldState& world,
+                                                            const PlannerConfig& cfg) {
+  const FieldGeometry& f = world.field;
+  if (!(pt.x >= 0.0 && pt.x <= 0.5 * f.length && std::fabs(pt.y) <= 0.5 * f.width))
+    throw domain_error("running point outside the front-field region");
+  if (f.strictly_in_their_defense_area(pt))
+    throw domain_error("guard points undefined: point inside the defense area");
+  pp_ctx* ctx = context();
+  const pp_world w = to_pp(world);
+  const pp_params p = to_pp(cfg);
+  double score;
+  pp_run_features feat;
+  uint8_t ok = 0;
+  check(pp_score_running_points(ctx, &w, &p, 1, &pt.x, &pt.y, &score, &feat, &ok), ctx);
+  if (!ok) throw domain_error("running point not scorable");
+  return {score, from_pp(feat)};
+}
+
+std::vector<RunningPoint> best_running_points(const WorldState& world,
+                                              const std::set<ZoneLabel>& occupied,
+                                              const PlannerConfig& cfg, int n_runners,
+                                              std::optional<Vec2> best_pass_point) {
+  (void)partition_zones(world.field, world.ball.position, cfg.thresholds.min_zone_width);
+  pp_ctx* ctx = context();
+  const pp_world w = to_pp(world);
+  const pp_params p = to_pp(cfg);
+  pp_runmap_request req{};
+  req.zone_mask = 0;
+  for (ZoneLabel z : occupied) req.occupied_mask |= 1u << static_cast<int>(z);
+  req.n_runners = n_runners;
+  req.has_best_pass_point = best_pass_point ? 1 : 0;
+  if (best_pass_point) {
+    req.best_pass_px = best_pass_point->x;
+    req.best_pass_py = best_pass_point->y;
+  }
+  req.want_map = 0;
+  void* block = host_block(pp_runmap_bytes(0));
+  check(pp_runmap(ctx, &w, &p, &req, block, 0), ctx);
+  pp_runmap_view v;
+  pp_runmap_view_of(block, 0, &v);
+  std::vector<RunningPoint> out;
+  for (int i = 0; i < v.summary->n_best; ++i) {
+    const pp_running_point& rp = v.summary->best[v.summary->best_order[i]];
+    out.push_back({static_cast<ZoneLabel>(rp.zone), {rp.px, rp.py}, rp.score, from_pp(rp.features)});
+  }
+  return out;
+}
+
+std::vector<FrameBest> best_pass_batch(const std::vector<WorldState>& frames,
+                                       const std::vector<int>& kicker_ids, const SearchGrid& grid,
+                                       const PlannerConfig& cfg) {
+  grid.validate();
+  cfg.validate();
+  pp_ctx* ctx = context();
+  std::vector<pp_world> w(frames.size());
+  for (size_t i = 0; i < frames.size(); ++i) w[i] = to_pp(frames[i]);
+  const pp_params p = to_pp(cfg);
+  const pp_search_grid g = to_pp(grid);
+  std::vector<pp_dpps_summary> sums(frames.size());
+  check(pp_dpps_batch(ctx, w.data(), static_cast<int64_t>(w.size()), &p, &g,
+                      kicker_ids.empty() ? nullptr : kicker_ids.data(), sums.data()),
+        ctx);
+  const int nd = grid.n_directions, np = grid.n_powers;
+  const auto kts = grid.kick_types();
+  std::vector<FrameBest> out(frames.size());
+  for (size_t i = 0; i < frames.size(); ++i) {
+    const pp_dpps_summary& s = sums[i];
+    out[i].n_feasible = s.n_feasible[0];
+    if (s.best_cell[0] < 0) continue;
+    const int64_t c = s.best_cell[0];
+    ScoredPass sp;
+    sp.candidate.kick_type = kts[static_cast<size_t>(c / (int64_t(nd) * np))];
+    sp.candidate.dir_index = static_cast<int>((c / np) % nd);
+    sp.candidate.power_index = static_cast<int>(c % np);
+    sp.candidate.our_time = s.best_features[0].teammate_intercept_time;
+    sp.candidate.feasible = true;
+    sp.score = s.best_score[0];
+    sp.features = from_pp(s.best_features[0]);
+    out[i].best = sp;
+  }
+  return out;
+}
+
+}  // namespace passplan

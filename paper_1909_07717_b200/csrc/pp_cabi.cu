@@ -771,6 +771,66 @@ struct RunSetup {
   int64_t n_map;
 };
 
+// Frame constants of score_running_point (offball.cpp:176-201), including the
+// point-independent parts hoisted per frame: nearest opponent to the ball
+// (offball.cpp:188-191) and the guard ranking (offball.cpp:143-155).
+void fill_run_common(const pp_world& w, const pp_params& p, pp::RunParams& R) {
+  const pp_field& f = w.field;
+  R.L = f.length;
+  R.W = f.width;
+  R.dd = f.defense_depth;
+  R.dw = f.defense_width;
+  R.gw = f.goal_width;
+  R.ball_x = w.ball_px;
+  R.ball_y = w.ball_py;
+  R.a_t = p.motion_theirs.max_accel;
+  R.b_t = p.motion_theirs.max_decel;
+  R.vmax_t = p.motion_theirs.max_speed;
+  R.cap = p.thresholds.guard_time_cap;
+  R.w_dg = p.run_weights.dist_goal;
+  R.w_db = p.run_weights.dist_ball;
+  R.w_angle = p.run_weights.angle;
+  R.w_guard = p.run_weights.guard_time;
+  R.w_exp = p.run_weights.exposure;
+  R.len_upper = p.norm.length_upper > 0.0 ? p.norm.length_upper : f.length;
+  R.band_full_lo = p.angle_band.full_lo;
+  R.band_peak_lo = p.angle_band.peak_lo;
+  R.band_peak_hi = p.angle_band.peak_hi;
+  R.band_full_hi = p.angle_band.full_hi;
+  double nearest = std::numeric_limits<double>::infinity();
+  for (int i = 0; i < w.n_theirs; ++i) {
+    const double d = host_distance(w.theirs[i].px, w.theirs[i].py, w.ball_px, w.ball_py);
+    nearest = std::min(nearest, d);
+  }
+  R.nearest_opp = nearest;
+  const double bx0 = 0.5 * f.length - f.defense_depth, bx1 = 0.5 * f.length;
+  const double by0 = -0.5 * f.defense_width, by1 = 0.5 * f.defense_width;
+  struct Cand {
+    double dist;
+    int id;
+    int idx;
+  };
+  std::vector<Cand> cands;
+  for (int i = 0; i < w.n_theirs; ++i) {
+    const pp_robot& r = w.theirs[i];
+    const double cx = std::clamp(r.px, bx0, bx1);
+    const double cy = std::clamp(r.py, by0, by1);
+    cands.push_back({host_distance(r.px, r.py, cx, cy), r.id, i});
+  }
+  std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
+    if (a.dist != b.dist) return a.dist < b.dist;
+    return a.id < b.id;
+  });
+  R.n_guards = static_cast<int32_t>(std::min<size_t>(cands.size(), 2));
+  for (int g = 0; g < R.n_guards; ++g) {
+    const pp_robot& r = w.theirs[cands[g].idx];
+    R.g_px[g] = r.px;
+    R.g_py[g] = r.py;
+    R.g_vx[g] = r.vx;
+    R.g_vy[g] = r.vy;
+  }
+}
+
 bool setup_runmap(const pp_world& w, const pp_params& p, const pp_runmap_request& req,
                   RunSetup* out, std::string* why) {
   const pp_field& f = w.field;
@@ -837,61 +897,7 @@ bool setup_runmap(const pp_world& w, const pp_params& p, const pp_runmap_request
   }
   out->n_map = at;
   R.step = step;
-  R.L = f.length;
-  R.W = f.width;
-  R.dd = f.defense_depth;
-  R.dw = f.defense_width;
-  R.gw = f.goal_width;
-  R.ball_x = w.ball_px;
-  R.ball_y = w.ball_py;
-  R.a_t = p.motion_theirs.max_accel;
-  R.b_t = p.motion_theirs.max_decel;
-  R.vmax_t = p.motion_theirs.max_speed;
-  R.cap = p.thresholds.guard_time_cap;
-  R.w_dg = p.run_weights.dist_goal;
-  R.w_db = p.run_weights.dist_ball;
-  R.w_angle = p.run_weights.angle;
-  R.w_guard = p.run_weights.guard_time;
-  R.w_exp = p.run_weights.exposure;
-  R.len_upper = p.norm.length_upper > 0.0 ? p.norm.length_upper : f.length;
-  R.band_full_lo = p.angle_band.full_lo;
-  R.band_peak_lo = p.angle_band.peak_lo;
-  R.band_peak_hi = p.angle_band.peak_hi;
-  R.band_full_hi = p.angle_band.full_hi;
-  // Point-independent parts hoisted per frame: nearest opponent to the ball
-  // (offball.cpp:188-191) and the guard ranking (offball.cpp:143-155).
-  double nearest = std::numeric_limits<double>::infinity();
-  for (int i = 0; i < w.n_theirs; ++i) {
-    const double d = host_distance(w.theirs[i].px, w.theirs[i].py, w.ball_px, w.ball_py);
-    nearest = std::min(nearest, d);
-  }
-  R.nearest_opp = nearest;
-  const double bx0 = 0.5 * f.length - f.defense_depth, bx1 = 0.5 * f.length;
-  const double by0 = -0.5 * f.defense_width, by1 = 0.5 * f.defense_width;
-  struct Cand {
-    double dist;
-    int id;
-    int idx;
-  };
-  std::vector<Cand> cands;
-  for (int i = 0; i < w.n_theirs; ++i) {
-    const pp_robot& r = w.theirs[i];
-    const double cx = std::clamp(r.px, bx0, bx1);
-    const double cy = std::clamp(r.py, by0, by1);
-    cands.push_back({host_distance(r.px, r.py, cx, cy), r.id, i});
-  }
-  std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
-    if (a.dist != b.dist) return a.dist < b.dist;
-    return a.id < b.id;
-  });
-  R.n_guards = static_cast<int32_t>(std::min<size_t>(cands.size(), 2));
-  for (int g = 0; g < R.n_guards; ++g) {
-    const pp_robot& r = w.theirs[cands[g].idx];
-    R.g_px[g] = r.px;
-    R.g_py[g] = r.py;
-    R.g_vx[g] = r.vx;
-    R.g_vy[g] = r.vy;
-  }
+  fill_run_common(w, p, R);
   (void)max_blocks;
   return true;
 }
@@ -973,6 +979,43 @@ pp_status pp_runmap(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   for (int z = 0; z < 4; ++z) {
     S.best_order[z] = -1;
     if (S.best[z].valid) S.best_order[S.n_best++] = z;
+  }
+  return PP_OK;
+}
+
+pp_status pp_score_running_points(pp_ctx* ctx, const pp_world* world, const pp_params* params,
+                                  int64_t n, const double* px, const double* py,
+                                  double* score_out, pp_run_features* features_out,
+                                  uint8_t* ok_out) {
+  if (!ctx || !world || !params) return fail(ctx, PP_INTERNAL, "null argument");
+  ctx->err.clear();
+  std::string why;
+  if (!validate_params(*params, &why)) return fail(ctx, PP_CONFIG, "%s", why.c_str());
+  if (n == 0) return PP_OK;
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  pp::RunParams R;
+  std::memset(&R, 0, sizeof(R));
+  fill_run_common(*world, *params, R);
+  std::vector<double> in(2 * static_cast<size_t>(n));
+  std::memcpy(in.data(), px, n * 8);
+  std::memcpy(in.data() + n, py, n * 8);
+  PP_CUDA_TRY(ctx, ctx->scratch_in.reserve(in.size() * 8));
+  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(7 * static_cast<size_t>(n) * 8));
+  cudaStream_t s = ctx->stream;
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->scratch_in.p, in.data(), in.size() * 8, cudaMemcpyHostToDevice, s));
+  const double* d = static_cast<const double*>(ctx->scratch_in.p);
+  pp::run_points_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(
+      R, n, d, d + n, static_cast<double*>(ctx->scratch_out.p));
+  PP_CUDA_TRY(ctx, cudaGetLastError());
+  std::vector<double> o(7 * static_cast<size_t>(n));
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(o.data(), ctx->scratch_out.p, o.size() * 8, cudaMemcpyDeviceToHost, s));
+  PP_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < n; ++i) {
+    if (ok_out) ok_out[i] = o[7 * i] != 0.0;
+    if (score_out) score_out[i] = o[7 * i + 1];
+    if (features_out)
+      features_out[i] = pp_run_features{o[7 * i + 2], o[7 * i + 3], o[7 * i + 4], o[7 * i + 5],
+                                        o[7 * i + 6]};
   }
   return PP_OK;
 }

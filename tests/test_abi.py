@@ -142,3 +142,19 @@ def test_world_struct_roundtrip(grids_golden):
     w, p, grid, k, st = case_inputs(grids_golden, "bench16")
     assert w.n_ours == 16 and w.n_theirs == 16 and st == 0
     assert grid.n_directions == 128 and grid.n_powers == 64
+
+
+def test_cpp_dropin_exports_reference_api():
+    """lib/libpassplan.so exports the reference's hot-path C++ entry points."""
+    from paper_1909_07717_b200 import build as b
+    lib = b.build_dropin()
+    out = subprocess.run(["nm", "-DC", "--defined-only", lib], capture_output=True,
+                         text=True).stdout
+    for sym in ("passplan::run_dpps(", "passplan::run_dpps_serial(", "passplan::best_pass(",
+                "passplan::score_pass(", "passplan::goal_view(", "passplan::shoot_angle(",
+                "passplan::score_running_point(", "passplan::best_running_points(",
+                "passplan::zone_lattice(", "passplan::partition_zones(",
+                "passplan::direction_table(", "passplan::power_table(",
+                "passplan::grids_identical(", "passplan::feasible_candidates(",
+                "passplan::PlannerConfig::validate() const", "passplan::best_pass_batch("):
+        assert sym in out, sym
