@@ -71,10 +71,11 @@ struct pp_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evm = nullptr;
   std::string err;
   // single frame
-  DevBuf frame, block, partials, counters, dirs, scratch_in, scratch_out;
+  DevBuf frame, block, partials, counters, dirs, pows, scratch_in, scratch_out;
   DevBuf queue, fcount;  // scan -> value pipeline (per-frame cell queues, counters)
   PinnedBuf frame_h;
   int dirs_n = -1;
+  std::vector<double> pows_key;  // inputs the power table was built from
   // run map
   DevBuf run_block, run_partials, run_counter;
   // batch
@@ -389,14 +390,73 @@ int32_t possession_of(const pp_world& w, int32_t kicker_id, const pp_params& p) 
   return host_distance(w.ball_px, w.ball_py, k->px, k->py) <= p.thresholds.possession_radius;
 }
 
-cudaError_t ensure_dirs(pp_ctx* ctx, int n) {
-  if (ctx->dirs_n == n) return cudaSuccess;
-  const std::vector<double> xy = direction_table(n);
-  cudaError_t e = ctx->dirs.reserve(xy.size() * sizeof(double));
-  if (e != cudaSuccess) return e;
-  e = cudaMemcpy(ctx->dirs.p, xy.data(), xy.size() * sizeof(double), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) ctx->dirs_n = n;
-  return e;
+// World-independent tables of a (params, grid): unit directions and the
+// per-(kick slot, power) trajectory rows.  Built on the host with the same
+// FP64 operations as the kernels (pp_math.cuh is host/device) and uploaded
+// only when the inputs change.  Fills P.dirs / P.pows.
+cudaError_t ensure_tables(pp_ctx* ctx, pp::DevParams* P) {
+  using pp::xd;
+  cudaError_t e = cudaSuccess;
+  if (ctx->dirs_n != P->n_dirs) {
+    const std::vector<double> xy = direction_table(P->n_dirs);
+    std::vector<double4> d(static_cast<size_t>(P->n_dirs));
+    for (int i = 0; i < P->n_dirs; ++i) {
+      const xd dx = xy[2 * i], dy = xy[2 * i + 1];
+      const xd n = pp::xsqrt(dx * dx + dy * dy);  // dpps.cpp:120-122 normalized()
+      xd ux = 1.0, uy = 0.0;
+      if (n.v != 0.0) {
+        ux = dx / n;
+        uy = dy / n;
+      }
+      d[i] = make_double4(dx.v, dy.v, ux.v, uy.v);
+    }
+    e = ctx->dirs.reserve(d.size() * sizeof(double4));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(ctx->dirs.p, d.data(), d.size() * sizeof(double4), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    ctx->dirs_n = P->n_dirs;
+    ctx->last_valid = false;
+  }
+  const std::vector<double> key = {P->slide, P->roll, P->ratio, P->chip_frac, P->dt,
+                                   P->power_min, P->power_max, double(P->n_pows),
+                                   double(P->n_kt), double(P->kt_chip0), double(P->kt_chip1)};
+  if (key != ctx->pows_key) {
+    std::vector<pp::PowRow> rows(static_cast<size_t>(P->n_kt) * P->n_pows);
+    const xd dt = P->dt, slide = P->slide, roll = P->roll;
+    for (int s = 0; s < P->n_kt; ++s) {
+      const bool chip = (s == 0 ? P->kt_chip0 : P->kt_chip1) != 0;
+      for (int pw = 0; pw < P->n_pows; ++pw) {
+        xd speed = P->power_min;  // power_table, dpps.cpp:50-62
+        if (P->n_pows > 1)
+          speed = xd(P->power_min) + (xd(double(pw)) * (xd(P->power_max) - xd(P->power_min))) /
+                                         xd(double(P->n_pows - 1));
+        const pp::Traj tr = pp::resolve_kick(speed, chip, slide, roll, P->ratio, P->chip_frac);
+        pp::PowRow& r = rows[static_cast<size_t>(s) * P->n_pows + pw];
+        r.speed = tr.speed.v;
+        r.v1 = tr.v1.v;
+        r.t_se = tr.t_se.v;
+        r.d_se = tr.d_se.v;
+        r.t_stop = tr.t_stop.v;
+        r.d_stop = tr.d_stop.v;
+        r.count = static_cast<int32_t>(std::floor((tr.t_stop / dt + xd(1e-9)).v)) + 1;
+        r.kb = 0;
+        if (tr.from.v > 0.0) {  // chip: skip the airborne stretch (intercept.cpp:47-69)
+          const xd t_air = pp::travel_time_to_distance(tr, slide, roll, tr.from);
+          if (!std::isnan(t_air.v)) r.kb = static_cast<int32_t>(std::ceil((t_air / dt - xd(1e-9)).v));
+        }
+      }
+    }
+    e = ctx->pows.reserve(rows.size() * sizeof(pp::PowRow));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(ctx->pows.p, rows.data(), rows.size() * sizeof(pp::PowRow),
+                     cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    ctx->pows_key = key;
+    ctx->last_valid = false;
+  }
+  P->dirs = static_cast<const double4*>(ctx->dirs.p);
+  P->pows = static_cast<const pp::PowRow*>(ctx->pows.p);
+  return cudaSuccess;
 }
 
 // Robots scanned per tile (passed on as the scan CTA width request).
@@ -443,17 +503,16 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   const int64_t chunks = chunks_for(P);
   const int n_scan = scan_threads / 32;
   const int64_t ctas = n_frames * P.n_tiles;
-  const double2* dirs = static_cast<const double2*>(ctx->dirs.p);
   // Latency (few tiles): one warp per robot.  Throughput (>= 2 waves of the
   // narrow shape): 4-warp CTAs, 8 per SM, robots round-robin over the warps.
   if (ctas >= 2 * 148 * pp::kScanCtasNarrow) {
     const int w = n_scan < pp::kScanWarpsNarrow ? n_scan : pp::kScanWarpsNarrow;
     pp::scan_kernel<kCells, pp::kScanWarpsNarrow, pp::kScanCtasNarrow>
-        <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, dirs, P, co, q, fc);
+        <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, P, co, q, fc);
   } else {
     const int w = n_scan < pp::kScanWarpsWide ? n_scan : pp::kScanWarpsWide;
     pp::scan_kernel<kCells, pp::kScanWarpsWide, pp::kScanCtasWide>
-        <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, dirs, P, co, q, fc);
+        <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, P, co, q, fc);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -617,8 +676,8 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
                       possession_of(*world, kicker_id, *params));
     return PP_OK;
   }
-  const pp::DevParams P = make_dev_params(*params, g);
-  PP_CUDA_TRY(ctx, ensure_dirs(ctx, g.n_directions));
+  pp::DevParams P = make_dev_params(*params, g);
+  PP_CUDA_TRY(ctx, ensure_tables(ctx, &P));
   PP_CUDA_TRY(ctx, ctx->block.reserve(off.total));
   PP_CUDA_TRY(ctx, reserve_pipeline(ctx, P, 1));
 
@@ -1073,8 +1132,8 @@ pp_status pp_batch_run(pp_ctx* ctx, const pp_params* params, const pp_search_gri
     if (device_ms) *device_ms = 0.f;
     return PP_OK;
   }
-  const pp::DevParams P = make_dev_params(*params, g);
-  PP_CUDA_TRY(ctx, ensure_dirs(ctx, g.n_directions));
+  pp::DevParams P = make_dev_params(*params, g);
+  PP_CUDA_TRY(ctx, ensure_tables(ctx, &P));
   int max_scan = 0;
   for (const auto& F : ctx->batch_host) max_scan = std::max(max_scan, F.n_scan);
   const int threads = 32 * warps_for(max_scan);
@@ -1159,5 +1218,23 @@ extern "C" int pp_debug_scan_counts(unsigned long long* out, int reset) {
     if (cudaMemcpyToSymbol(pp::g_scan_counts, z, sizeof(z)) != cudaSuccess) return PP_CUDA;
   }
   return PP_OK;
+}
+#endif
+
+#ifdef PP_PHASE_CLOCKS
+// Profiling build only: per-CTA records of the last launches (see PP_FLUSH).
+extern "C" int pp_debug_cta_records(long long* scan, long long* value, long long* robots) {
+  if (cudaMemcpyFromSymbol(scan, pp::g_cta_rec, sizeof(pp::g_cta_rec) / 2) != cudaSuccess ||
+      cudaMemcpyFromSymbol(value, pp::g_cta_rec, sizeof(pp::g_cta_rec) / 2, sizeof(pp::g_cta_rec) / 2) != cudaSuccess ||
+      cudaMemcpyFromSymbol(robots, pp::g_robot_rec, sizeof(pp::g_robot_rec)) != cudaSuccess)
+    return PP_CUDA;
+  return PP_OK;
+}
+#endif
+
+#ifdef PP_PHASE_CLOCKS
+extern "C" int pp_debug_lane_records(int* out) {
+  return cudaMemcpyFromSymbol(out, pp::g_lane_rec, sizeof(pp::g_lane_rec)) == cudaSuccess ? PP_OK
+                                                                                          : PP_CUDA;
 }
 #endif

@@ -13,35 +13,51 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <cmath>
+
+#define PP_HD __host__ __device__ __forceinline__
+
 namespace pp {
 
 struct xd {
   double v;
-  __host__ __device__ __forceinline__ xd() : v(0.0) {}
-  __host__ __device__ __forceinline__ xd(double x) : v(x) {}  // NOLINT(implicit)
+  PP_HD xd() : v(0.0) {}
+  PP_HD xd(double x) : v(x) {}  // NOLINT(implicit)
 };
 
-__device__ __forceinline__ xd operator+(xd a, xd b) { return __dadd_rn(a.v, b.v); }
-__device__ __forceinline__ xd operator-(xd a, xd b) { return __dsub_rn(a.v, b.v); }
-__device__ __forceinline__ xd operator*(xd a, xd b) { return __dmul_rn(a.v, b.v); }
-__device__ __forceinline__ xd operator/(xd a, xd b) { return __ddiv_rn(a.v, b.v); }
-__device__ __forceinline__ xd operator-(xd a) { return -a.v; }
-__device__ __forceinline__ bool operator<(xd a, xd b) { return a.v < b.v; }
-__device__ __forceinline__ bool operator>(xd a, xd b) { return a.v > b.v; }
-__device__ __forceinline__ bool operator<=(xd a, xd b) { return a.v <= b.v; }
-__device__ __forceinline__ bool operator>=(xd a, xd b) { return a.v >= b.v; }
-__device__ __forceinline__ bool operator==(xd a, xd b) { return a.v == b.v; }
-__device__ __forceinline__ xd xsqrt(xd a) { return __dsqrt_rn(a.v); }
-__device__ __forceinline__ xd xfabs(xd a) { return fabs(a.v); }
+// Device: the _rn intrinsics (never contracted).  Host (compiled with
+// -ffp-contract=off): plain IEEE operations -- the same correctly rounded
+// results, so host-precomputed tables equal what the kernels would compute.
+#ifdef __CUDA_ARCH__
+PP_HD xd operator+(xd a, xd b) { return __dadd_rn(a.v, b.v); }
+PP_HD xd operator-(xd a, xd b) { return __dsub_rn(a.v, b.v); }
+PP_HD xd operator*(xd a, xd b) { return __dmul_rn(a.v, b.v); }
+PP_HD xd operator/(xd a, xd b) { return __ddiv_rn(a.v, b.v); }
+PP_HD xd xsqrt(xd a) { return __dsqrt_rn(a.v); }
+#else
+PP_HD xd operator+(xd a, xd b) { return a.v + b.v; }
+PP_HD xd operator-(xd a, xd b) { return a.v - b.v; }
+PP_HD xd operator*(xd a, xd b) { return a.v * b.v; }
+PP_HD xd operator/(xd a, xd b) { return a.v / b.v; }
+PP_HD xd xsqrt(xd a) { return std::sqrt(a.v); }
+#endif
+PP_HD xd operator-(xd a) { return -a.v; }
+PP_HD bool operator<(xd a, xd b) { return a.v < b.v; }
+PP_HD bool operator>(xd a, xd b) { return a.v > b.v; }
+PP_HD bool operator<=(xd a, xd b) { return a.v <= b.v; }
+PP_HD bool operator>=(xd a, xd b) { return a.v >= b.v; }
+PP_HD bool operator==(xd a, xd b) { return a.v == b.v; }
+constexpr double kInfD = __builtin_huge_val();
+PP_HD xd xfabs(xd a) { return fabs(a.v); }
 
 // ---- vec2.hpp:22-56 ----------------------------------------------------
-__device__ __forceinline__ xd dist2d(xd ax, xd ay, xd bx, xd by) {
+PP_HD xd dist2d(xd ax, xd ay, xd bx, xd by) {
   const xd dx = ax - bx, dy = ay - by;  // (a - b).norm()
   return xsqrt(dx * dx + dy * dy);
 }
 
 // segment_distance(p, a, b), vec2.hpp:48-56.
-__device__ __forceinline__ xd segment_distance(xd px, xd py, xd ax, xd ay, xd bx, xd by) {
+PP_HD xd segment_distance(xd px, xd py, xd ax, xd ay, xd bx, xd by) {
   const xd abx = bx - ax, aby = by - ay;
   const xd len2 = abx * abx + aby * aby;
   if (len2.v == 0.0) return dist2d(px, py, ax, ay);
@@ -52,7 +68,7 @@ __device__ __forceinline__ xd segment_distance(xd px, xd py, xd ax, xd ay, xd bx
 }
 
 // ---- detail/arrival_math.hpp:15-69 --------------------------------------
-__device__ __forceinline__ xd rest_to_rest_time(xd L, xd a, xd b, xd vmax) {
+PP_HD xd rest_to_rest_time(xd L, xd a, xd b, xd vmax) {
   const xd peak2 = ((xd(2.0) * a) * b * L) / (a + b);
   const xd peak = xsqrt(peak2);
   if (peak <= vmax) return peak / a + peak / b;
@@ -60,7 +76,7 @@ __device__ __forceinline__ xd rest_to_rest_time(xd L, xd a, xd b, xd vmax) {
   return vmax / a + vmax / b + (L - d_used) / vmax;
 }
 
-__device__ __forceinline__ xd one_d_time_to_rest(xd v0, xd dist, xd a, xd b, xd vmax) {
+PP_HD xd one_d_time_to_rest(xd v0, xd dist, xd a, xd b, xd vmax) {
   const xd brake_dist = (v0 * v0) / (xd(2.0) * b);
   if (v0.v < 0.0 || brake_dist > dist) {
     const xd gap = brake_dist - xd(copysign(dist.v, v0.v));
@@ -77,7 +93,7 @@ __device__ __forceinline__ xd one_d_time_to_rest(xd v0, xd dist, xd a, xd b, xd 
   return (v0 - vmax) / b + vmax / b + (dist - d_used) / vmax;
 }
 
-__device__ __forceinline__ xd arrival_given(xd qx, xd qy, xd d2, xd vx, xd vy, xd a, xd b,
+PP_HD xd arrival_given(xd qx, xd qy, xd d2, xd vx, xd vy, xd a, xd b,
                                             xd vmax, xd radius) {
   const xd d = xsqrt(d2);
   const xd deff_raw = d - radius;
@@ -92,7 +108,7 @@ __device__ __forceinline__ xd arrival_given(xd qx, xd qy, xd d2, xd vx, xd vy, x
   return t_along > t_cross ? t_along : t_cross;
 }
 
-__device__ __forceinline__ xd arrival_to_point(xd tx, xd ty, xd px, xd py, xd vx, xd vy, xd a,
+PP_HD xd arrival_to_point(xd tx, xd ty, xd px, xd py, xd vx, xd vy, xd a,
                                                xd b, xd vmax, xd radius) {
   const xd qx = tx - px;
   const xd qy = ty - py;
@@ -100,7 +116,7 @@ __device__ __forceinline__ xd arrival_to_point(xd tx, xd ty, xd px, xd py, xd vx
 }
 
 // arrival_time(robot, target, limits), motion.cpp:16-29 (radius 0).
-__device__ __forceinline__ xd arrival_time(xd px, xd py, xd vx, xd vy, xd tx, xd ty, xd a, xd b,
+PP_HD xd arrival_time(xd px, xd py, xd vx, xd vy, xd tx, xd ty, xd a, xd b,
                                            xd vmax) {
   const xd qx = tx - px;
   const xd qy = ty - py;
@@ -117,7 +133,7 @@ struct Traj {
   xd speed, v1, t_se, d_se, t_stop, d_stop, from;  // from = interceptable_from
 };
 
-__device__ __forceinline__ Traj resolve_kick(xd speed, bool chip, xd slide, xd roll, xd ratio,
+PP_HD Traj resolve_kick(xd speed, bool chip, xd slide, xd roll, xd ratio,
                                              xd chip_frac) {
   Traj t;
   t.speed = speed;
@@ -130,7 +146,7 @@ __device__ __forceinline__ Traj resolve_kick(xd speed, bool chip, xd slide, xd r
   return t;
 }
 
-__device__ __forceinline__ xd distance_at(const Traj& tr, xd slide, xd roll, xd t) {
+PP_HD xd distance_at(const Traj& tr, xd slide, xd roll, xd t) {
   if (t < tr.t_se) return tr.speed * t - xd(0.5) * slide * t * t;
   if (t < tr.t_stop) {
     const xd u = t - tr.t_se;
@@ -140,9 +156,9 @@ __device__ __forceinline__ xd distance_at(const Traj& tr, xd slide, xd roll, xd 
 }
 
 // travel_time_to_distance; returns NaN for nullopt (d beyond the rollout).
-__device__ __forceinline__ xd travel_time_to_distance(const Traj& tr, xd slide, xd roll, xd d) {
+PP_HD xd travel_time_to_distance(const Traj& tr, xd slide, xd roll, xd d) {
   if (d.v == 0.0) return 0.0;
-  if (d > tr.d_stop) return CUDART_NAN;
+  if (d > tr.d_stop) return __builtin_nan("");
   if (d <= tr.d_se) {
     const xd rad = tr.speed * tr.speed - xd(2.0) * slide * d;
     return xd(2.0) * d / (tr.speed + xsqrt(rad.v < 0.0 ? xd(0.0) : rad));
@@ -154,12 +170,12 @@ __device__ __forceinline__ xd travel_time_to_distance(const Traj& tr, xd slide, 
 
 // ray_exit_distance, intercept.cpp:27-43.  Returns NaN when the origin is
 // outside the field (nullopt).
-__device__ __forceinline__ xd ray_exit_distance(xd L, xd W, xd ox, xd oy, xd ux, xd uy) {
+PP_HD xd ray_exit_distance(xd L, xd W, xd ox, xd oy, xd ux, xd uy) {
   const xd hx = xd(0.5) * L;
   const xd hy = xd(0.5) * W;
-  if (!(ox.v >= -hx.v && ox.v <= hx.v && oy.v >= -hy.v && oy.v <= hy.v)) return CUDART_NAN;
+  if (!(ox.v >= -hx.v && ox.v <= hx.v && oy.v >= -hy.v && oy.v <= hy.v)) return __builtin_nan("");
   // std::min(a, b) == (b < a ? b : a); std::max(a, b) == (a < b ? b : a).
-  xd s_exit = CUDART_INF;
+  xd s_exit = kInfD;
   auto take_min = [&](xd c) { if (c < s_exit) s_exit = c; };
   if (ux.v > 0.0) {
     take_min((hx - ox) / ux);
@@ -174,6 +190,6 @@ __device__ __forceinline__ xd ray_exit_distance(xd L, xd W, xd ox, xd oy, xd ux,
   return s_exit.v < 0.0 ? xd(0.0) : s_exit;
 }
 
-__device__ __forceinline__ xd clamp01(xd x) { return x.v < 0.0 ? xd(0.0) : (x.v > 1.0 ? xd(1.0) : x); }
+PP_HD xd clamp01(xd x) { return x.v < 0.0 ? xd(0.0) : (x.v > 1.0 ? xd(1.0) : x); }
 
 }  // namespace pp
