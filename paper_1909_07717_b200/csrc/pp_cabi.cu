@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -478,6 +479,8 @@ cudaError_t reserve_pipeline(pp_ctx* ctx, const pp::DevParams& P, int64_t n_fram
   return ctx->partials.reserve(sizeof(pp::Partial) * static_cast<size_t>(n_frames * chunks_for(P)));
 }
 
+
+
 pp::CellQueue make_queue(pp_ctx* ctx, const pp::DevParams& P, int64_t n_frames) {
   const int64_t n_cells = static_cast<int64_t>(P.n_kt) * P.n_dirs * P.n_pows;
   const size_t n = static_cast<size_t>(n_frames * n_cells);
@@ -498,14 +501,14 @@ template <bool kCells>
 cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_frames,
                             const pp::DevParams& P, int scan_threads, const pp::CellOut& co,
                             pp_dpps_summary* sums, cudaEvent_t mid = nullptr) {
+  const int n_scan = scan_threads / 32;
+  const int64_t ctas = n_frames * P.n_tiles;
   const pp::CellQueue q = make_queue(ctx, P, n_frames);
   auto* fc = static_cast<pp::FrameCounters*>(ctx->fcount.p);
   const int64_t chunks = chunks_for(P);
-  const int n_scan = scan_threads / 32;
-  const int64_t ctas = n_frames * P.n_tiles;
-  // Latency (few tiles): one warp per robot.  Throughput (>= 2 waves of the
-  // narrow shape): 4-warp CTAs, 8 per SM, robots round-robin over the warps.
   if (ctas >= 2 * 148 * pp::kScanCtasNarrow) {
+    // Throughput (>= 2 waves of the narrow shape): 4-warp CTAs, 8 per SM,
+    // robots round-robin over the warps.
     const int w = n_scan < pp::kScanWarpsNarrow ? n_scan : pp::kScanWarpsNarrow;
     pp::scan_kernel<kCells, pp::kScanWarpsNarrow, pp::kScanCtasNarrow>
         <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, P, co, q, fc);
@@ -517,10 +520,17 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (mid) cudaEventRecord(mid, ctx->stream);
-  pp::value_kernel<kCells><<<static_cast<unsigned>(n_frames * chunks), pp::kValueThreads, 0,
-                             ctx->stream>>>(frames, P, q, fc, co,
-                                            static_cast<pp::Partial*>(ctx->partials.p), sums,
-                                            static_cast<int>(chunks));
+  // Few chunks (one frame): wider CTAs shorten each chunk's chain of
+  // dependent items; many chunks: narrower CTAs pack the SMs better.
+  const unsigned vctas = static_cast<unsigned>(n_frames * chunks);
+  auto* parts = static_cast<pp::Partial*>(ctx->partials.p);
+  if (vctas <= 4u * 148u) {
+    pp::value_kernel<kCells, pp::kValueThreadsWide><<<vctas, pp::kValueThreadsWide, 0, ctx->stream>>>(
+        frames, P, q, fc, co, parts, sums, static_cast<int>(chunks));
+  } else {
+    pp::value_kernel<kCells, pp::kValueThreads><<<vctas, pp::kValueThreads, 0, ctx->stream>>>(
+        frames, P, q, fc, co, parts, sums, static_cast<int>(chunks));
+  }
   return cudaGetLastError();
 }
 
@@ -1236,5 +1246,19 @@ extern "C" int pp_debug_cta_records(long long* scan, long long* value, long long
 extern "C" int pp_debug_lane_records(int* out) {
   return cudaMemcpyFromSymbol(out, pp::g_lane_rec, sizeof(pp::g_lane_rec)) == cudaSuccess ? PP_OK
                                                                                           : PP_CUDA;
+}
+#endif
+
+
+#ifdef PP_PHASE_CLOCKS
+extern "C" int pp_debug_edges(int* out, unsigned* n, int reset) {
+  if (cudaMemcpyFromSymbol(n, pp::g_edge_n, sizeof(unsigned)) != cudaSuccess ||
+      cudaMemcpyFromSymbol(out, pp::g_edge_rec, sizeof(pp::g_edge_rec)) != cudaSuccess)
+    return PP_CUDA;
+  if (reset) {
+    const unsigned z = 0;
+    if (cudaMemcpyToSymbol(pp::g_edge_n, &z, sizeof(z)) != cudaSuccess) return PP_CUDA;
+  }
+  return PP_OK;
 }
 #endif

@@ -95,3 +95,19 @@ for i in top:
 # by robot
 print("per robot mean cycles:", np.round(R.mean(0)).astype(int).tolist())
 print("per robot mean maxsteps:", np.round(it.max(-1).mean(0), 1).tolist())
+
+# goal-view edge bisections of one more chip=1 frame
+lib.pp_debug_edges.argtypes = [C.POINTER(C.c_int), C.POINTER(C.c_uint), C.c_int]
+E = np.zeros((1 << 15, 4), np.int32)
+ne = C.c_uint()
+lib.pp_debug_edges(E.ctypes.data_as(C.POINTER(C.c_int)), C.byref(ne), 1)
+grid.chip = 1
+blk = abi.GridBlock(128 * 64 * 2)
+lib.pp_dpps(ctx, C.byref(w), C.byref(p), C.byref(grid), k, 1, blk.ptr())
+lib.pp_debug_edges(E.ctypes.data_as(C.POINTER(C.c_int)), C.byref(ne), 1)
+E = E[:ne.value]
+print(f"edges {len(E)}: fast {E[:, 0].mean():.2f} iters {pct(E[:, 1])} exact {pct(E[:, 2])} cyc {pct(E[:, 3])}")
+for fl in (0, 1):
+    m = E[:, 0] == fl
+    if m.any():
+        print(f"  fast={fl}: n={m.sum()} iters {pct(E[m, 1])} exact {pct(E[m, 2])} cyc {pct(E[m, 3])}")

@@ -24,6 +24,10 @@ CHAIN(fdiv, float, 1.0f, x = y / x)
 CHAIN(fsqrt, float, 2.0f, x = sqrtf(x + 1.0f))
 CHAIN(frsq, float, 2.0f, x = rsqrtf(x) + 1.0f)
 CHAIN(datan2, double, 0.5, x = atan2(x, y) + 0.5)
+// compare-dependent chains: the select consumes the predicate
+CHAIN(dsetp, double, 1.0, x = (x < y) ? __dadd_rn(x, 1e-9) : __dsub_rn(x, 1e-9))
+CHAIN(fsetp, float, 1.0f, x = (x < y) ? __fadd_rn(x, 1e-7f) : __fsub_rn(x, 1e-7f))
+CHAIN(dmidp, double, 1.0, x = __dmul_rn(0.5, __dadd_rn(x, y)); x = (x == y) ? 1.0 : x)
 
 template <typename T>
 void run(const char* name, void (*k)(T*, long long*, int), int warps) {
@@ -49,6 +53,9 @@ int main() {
     run<double>("ddiv", k_ddiv, w);
     run<double>("dsqrt", k_dsqrt, w);
     run<double>("datan2", k_datan2, w);
+    run<double>("dsetp", k_dsetp, w);
+    run<double>("dmidp", k_dmidp, w);
+    run<float>("fsetp", k_fsetp, w);
     run<float>("fadd", k_fadd, w);
     run<float>("ffma", k_ffma, w);
     run<float>("fdiv", k_fdiv, w);
