@@ -147,7 +147,8 @@ typedef struct pp_dpps_summary {
   int64_t best_cell[3];            /* best_pass all / flat / chip; -1 = nullopt */
   double best_score[3];
   pp_pass_features best_features[3];
-  double device_ms;                /* kernel time of this frame (events) */
+  double device_ms;                /* kernel span of this frame on the device, ms
+                                      (first scan CTA start -> final fold) */
 } pp_dpps_summary;
 
 typedef struct pp_grid_view { /* typed pointers into a result block */

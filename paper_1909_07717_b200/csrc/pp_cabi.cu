@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -70,6 +71,10 @@ struct pp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evm = nullptr;
+  // pp_dpps as one CUDA graph (H2D frame, scan, value, D2H), rebuilt when
+  // its key (params, output pointers, copy flags, ...) changes.
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<unsigned char> gkey;
   std::string err;
   // single frame
   DevBuf frame, block, partials, counters, dirs, pows, scratch_in, scratch_out;
@@ -375,12 +380,20 @@ void fill_summary_host(pp_dpps_summary* s, const pp_world& w, const pp_search_gr
   s->kicker_in_possession = possession;
   s->n_ours = w.n_ours;
   s->n_theirs = w.n_theirs;
-  const std::vector<int> so = id_order(w.ours, w.n_ours);
-  const std::vector<int> st = id_order(w.theirs, w.n_theirs);
-  for (int i = 0; i < PP_MAX_TEAM; ++i) {
-    s->ours_ids[i] = i < w.n_ours ? w.ours[so[i]].id : -1;
-    s->theirs_ids[i] = i < w.n_theirs ? w.theirs[st[i]].id : -1;
-  }
+  // id-sorted teams (stable insertion sort: at most 16 robots, no allocation)
+  auto sorted_ids = [](const pp_robot* r, int n, int32_t* out) {
+    for (int i = 0; i < PP_MAX_TEAM; ++i) out[i] = -1;
+    for (int i = 0; i < n && i < PP_MAX_TEAM; ++i) {
+      int j = i;
+      while (j > 0 && out[j - 1] > r[i].id) {
+        out[j] = out[j - 1];
+        --j;
+      }
+      out[j] = r[i].id;
+    }
+  };
+  sorted_ids(w.ours, w.n_ours, s->ours_ids);
+  sorted_ids(w.theirs, w.n_theirs, s->theirs_ids);
   s->sbip_calls = static_cast<uint64_t>(s->n_cells) *
                   static_cast<uint64_t>(w.n_ours + w.n_theirs);  // dpps.cpp:148-153
 }
@@ -542,6 +555,28 @@ cudaError_t launch_single(pp_ctx* ctx, cudaEvent_t mid = nullptr) {
 
 }  // namespace
 
+
+// Dev-only host stage timing of pp_dpps (PP_HOST_TRACE=1): mean microseconds
+// between stages, printed to stderr every 1000 calls.
+static bool g_ht_on = std::getenv("PP_HOST_TRACE") != nullptr;
+static double g_ht_acc[8];
+static std::chrono::steady_clock::time_point g_ht_last;
+static int g_ht_n = 0;
+#define HT(k)                                                                   \
+  if (g_ht_on) {                                                                \
+    const auto now_ = std::chrono::steady_clock::now();                         \
+    if (k > 0) g_ht_acc[k] += std::chrono::duration<double, std::micro>(now_ - g_ht_last).count(); \
+    g_ht_last = now_;                                                           \
+  }
+static void ht_flush() {
+  if (!g_ht_on || ++g_ht_n < 200) return;
+  std::fprintf(stderr, "pp_dpps host stages (us):");
+  for (int i = 1; i < 7; ++i) std::fprintf(stderr, " %.2f", g_ht_acc[i] / g_ht_n);
+  std::fprintf(stderr, "\n");
+  for (double& a : g_ht_acc) a = 0.0;
+  g_ht_n = 0;
+}
+
 extern "C" {
 
 int pp_abi_version(void) { return PP_ABI_VERSION; }
@@ -654,6 +689,7 @@ void pp_ctx_destroy(pp_ctx* ctx) {
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->evm) cudaEventDestroy(ctx->evm);
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -664,6 +700,7 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
                   const pp_search_grid* grid_in, int32_t kicker_id, uint32_t copy_flags,
                   void* block) {
   if (!ctx || !world || !params || !block) return fail(ctx, PP_INTERNAL, "null argument");
+  HT(0);
   ctx->err.clear();
   const pp_search_grid& g = grid_in ? *grid_in : params->grid;
   std::string why;
@@ -675,6 +712,7 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   if (!pack_frame(*world, kicker_id, F, &kicker_slot, &why))
     return fail(ctx, PP_VALIDATION, "%s", why.c_str());
 
+  HT(1);
   const int64_t n_cells = pp_grid_cells(&g);
   const pp_grid_offsets_ off = pp_grid_offsets_for_(n_cells);
   pp_grid_view hv;
@@ -690,6 +728,7 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   PP_CUDA_TRY(ctx, ensure_tables(ctx, &P));
   PP_CUDA_TRY(ctx, ctx->block.reserve(off.total));
   PP_CUDA_TRY(ctx, reserve_pipeline(ctx, P, 1));
+  HT(2);
 
   char* dblk = static_cast<char*>(ctx->block.p);
   pp::CellOut co;
@@ -704,23 +743,106 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   pp_dpps_summary* dsum = reinterpret_cast<pp_dpps_summary*>(dblk + off.summary);
 
   cudaStream_t s = ctx->stream;
-  PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->frame.p, F, sizeof(pp::FrameDev), cudaMemcpyHostToDevice, s));
-  PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, s));
   ctx->last_P = P;
   ctx->last_co = co;
   ctx->last_dsum = dsum;
   ctx->last_threads = 32 * warps_for(F->n_scan);
   ctx->last_valid = true;
-  PP_CUDA_TRY(ctx, launch_single(ctx));
-  PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, s));
-  const size_t bytes = (copy_flags & PP_COPY_ALL) ? off.total : sizeof(pp_dpps_summary);
-  PP_CUDA_TRY(ctx, cudaMemcpyAsync(block, dblk, bytes, cudaMemcpyDeviceToHost, s));
+  const bool all = (copy_flags & PP_COPY_ALL) != 0;
+  char* hblk = static_cast<char*>(block);
+  // A pinned block (pp_host_alloc) is device-addressable: the scan kernel
+  // then writes the per-cell outputs straight into it over PCIe while it
+  // runs, and only the score array and the summary are copied afterwards.
+  bool pinned = false;
+  {
+    cudaPointerAttributes pa{};
+    pinned = cudaPointerGetAttributes(&pa, block) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+             pa.devicePointer == block;
+    cudaGetLastError();
+  }
+  const bool direct = all && pinned;
+  pp::CellOut co_run = co;
+  if (direct) {
+    co_run.our_time = reinterpret_cast<double*>(hblk + off.our_time);
+    co_run.opp_time = reinterpret_cast<double*>(hblk + off.opp_time);
+    co_run.rx = reinterpret_cast<double*>(hblk + off.rx);
+    co_run.ry = reinterpret_cast<double*>(hblk + off.ry);
+    co_run.our_slot = reinterpret_cast<int8_t*>(hblk + off.our_slot);
+    co_run.opp_slot = reinterpret_cast<int8_t*>(hblk + off.opp_slot);
+    co_run.feasible = reinterpret_cast<uint8_t*>(hblk + off.feasible);
+  }
+  HT(3);
+  // (summary.device_ms is the kernels' own span, measured on the device)
+  auto enqueue = [&]() -> cudaError_t {
+    cudaError_t e = cudaMemcpyAsync(ctx->frame.p, F, sizeof(pp::FrameDev), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+      e = launch_pipeline<true>(ctx, static_cast<const pp::FrameDev*>(ctx->frame.p), 1, P,
+                                ctx->last_threads, co_run, dsum);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(block, dblk, sizeof(pp_dpps_summary), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && direct)
+      e = cudaMemcpyAsync(hblk + off.score, dblk + off.score, off.our_slot - off.score,
+                          cudaMemcpyDeviceToHost, s);
+    else if (e == cudaSuccess && all)
+      e = cudaMemcpyAsync(hblk + off.our_time, dblk + off.our_time, off.total - off.our_time,
+                          cudaMemcpyDeviceToHost, s);
+    return e;
+  };
+  if (!pinned) {  // pageable block: plain stream work (graphs copy pinned memory only)
+    PP_CUDA_TRY(ctx, enqueue());
+    PP_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  } else {
+  // The whole call is one graph: H2D frame -> scan -> value -> D2H.
+  struct Key {
+    pp::DevParams P;
+    pp::CellOut co;
+    const void* block;
+    const void* dblk;
+    const void* bufs[4];  // pipeline buffers baked into the graph
+    int64_t n_cells;
+    uint32_t flags;
+    int32_t threads, direct;
+  } key;
+  std::memset(&key, 0, sizeof(key));
+  key.P = P;
+  key.co = co_run;
+  key.block = block;
+  key.dblk = dblk;
+  key.bufs[0] = ctx->queue.p;
+  key.bufs[1] = ctx->fcount.p;
+  key.bufs[2] = ctx->partials.p;
+  key.bufs[3] = ctx->frame.p;
+  key.n_cells = n_cells;
+  key.flags = copy_flags;
+  key.threads = ctx->last_threads;
+  key.direct = direct;
+  const unsigned char* kb = reinterpret_cast<const unsigned char*>(&key);
+  if (!ctx->gexec || ctx->gkey.size() != sizeof(key) ||
+      std::memcmp(ctx->gkey.data(), kb, sizeof(key)) != 0) {
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+    ctx->gkey.clear();
+    PP_CUDA_TRY(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = enqueue();
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e2 = cudaStreamEndCapture(s, &graph);
+    if (e == cudaSuccess) e = e2;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&ctx->gexec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    PP_CUDA_TRY(ctx, e);
+    ctx->gkey.assign(kb, kb + sizeof(key));
+  }
+  HT(4);
+  PP_CUDA_TRY(ctx, cudaGraphLaunch(ctx->gexec, s));
   PP_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  }
+  HT(5);
+  const double dms = hv.summary->device_ms;
   fill_summary_host(hv.summary, *world, g, kicker_id, kicker_slot,
                     possession_of(*world, kicker_id, *params));
-  hv.summary->device_ms = ms;
+  hv.summary->device_ms = dms;
+  HT(6);
+  ht_flush();
   return PP_OK;
 }
 

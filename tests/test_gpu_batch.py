@@ -31,7 +31,7 @@ def test_batch_equals_single_frame(ctx, chip):
     for i in range(n):
         k = int(sums[i].kicker_id)
         st, blk = run_product(lib, ctx, frames[i], p, grid, k, copy_all=False)
-        assert st == 0
+        assert st == 0, lib.pp_last_error(ctx)
         for r in range(3):
             assert sums[i].best_cell[r] == blk.summary.best_cell[r], (i, r)
             assert sums[i].best_score[r] == blk.summary.best_score[r], (i, r)
