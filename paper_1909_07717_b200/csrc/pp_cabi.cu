@@ -537,14 +537,26 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   // dependent items; many chunks: narrower CTAs pack the SMs better.
   const unsigned vctas = static_cast<unsigned>(n_frames * chunks);
   auto* parts = static_cast<pp::Partial*>(ctx->partials.p);
+  // Programmatic dependent launch: the value grid is launched while the scan
+  // grid drains and waits on it in-kernel (griddepcontrol.wait).
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(vctas);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = ctx->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = mid ? 0 : 1;  // (kernel timing splits the two grids)
+  const int nch = static_cast<int>(chunks);
   if (vctas <= 4u * 148u) {
-    pp::value_kernel<kCells, pp::kValueThreadsWide><<<vctas, pp::kValueThreadsWide, 0, ctx->stream>>>(
-        frames, P, q, fc, co, parts, sums, static_cast<int>(chunks));
-  } else {
-    pp::value_kernel<kCells, pp::kValueThreads><<<vctas, pp::kValueThreads, 0, ctx->stream>>>(
-        frames, P, q, fc, co, parts, sums, static_cast<int>(chunks));
+    cfg.blockDim = dim3(pp::kValueThreadsWide);
+    return cudaLaunchKernelEx(&cfg, pp::value_kernel<kCells, pp::kValueThreadsWide>, frames, P, q,
+                              fc, co, parts, sums, nch);
   }
-  return cudaGetLastError();
+  cfg.blockDim = dim3(pp::kValueThreads);
+  return cudaLaunchKernelEx(&cfg, pp::value_kernel<kCells, pp::kValueThreads>, frames, P, q, fc,
+                            co, parts, sums, nch);
 }
 
 // The single-frame launch of the last pp_dpps call.
