@@ -301,6 +301,73 @@ pp_status pp_batch_run(pp_ctx* ctx, const pp_params* params, const pp_search_gri
                        float* device_ms);
 pp_status pp_batch_download(pp_ctx* ctx, pp_dpps_summary* summaries);
 
+/* ---- interception, possession, shot decision, free kick ----------------
+ * (SURVEY §8(f) rows 2-4.)  One trajectory against robots, one warp per
+ * robot scanning 32 samples per step on the device. */
+
+typedef struct pp_kick { /* BallTrajectory::{flat_kick,chip_kick,free_roll}, ball_model.hpp:43-52 */
+  double origin_x, origin_y;
+  double dir_x, dir_y; /* kick direction; for a free roll the ball velocity */
+  double speed;        /* kick speed; ignored for a free roll (|velocity|) */
+  int32_t kind;        /* 0 flat kick, 1 chip kick, 2 free roll */
+  int32_t pad;
+} pp_kick;
+
+typedef struct pp_intercept { /* InterceptResult, intercept.hpp:13-20 */
+  int32_t team;     /* 0 ours, 1 theirs */
+  int32_t robot_id;
+  int32_t finite;   /* 0 = Never (intercept_time nullopt) */
+  int32_t pad;
+  double time, point_x, point_y;
+} pp_intercept;
+
+/* intercept_all (intercept.hpp:50-53, intercept.cpp:167-196): out[] gets
+ * n_ours + n_theirs results, ours then theirs, each team in id order.
+ * dt <= 0 -> PP_DOMAIN; invalid ball model -> PP_CONFIG. */
+pp_status pp_intercept_all(pp_ctx* ctx, const pp_world* world, const pp_params* params,
+                           const pp_kick* kick, double dt, pp_intercept* out);
+
+typedef struct pp_possession_report { /* PossessionReport, pass_eval.hpp:93-99 */
+  int32_t side; /* 0 ours, 1 theirs, 2 contested */
+  int32_t has_our, has_their, pad;
+  double our_time, their_time;
+} pp_possession_report;
+
+/* possession (pass_eval.cpp:271-298): the ball's free roll sampled at
+ * thresholds.possession_dt against both teams. */
+pp_status pp_possession(pp_ctx* ctx, const pp_world* world, const pp_params* params,
+                        pp_possession_report* out);
+
+typedef struct pp_shot_decision { /* ShotDecision, pass_eval.hpp:62-70 */
+  int32_t shoot, blocked;
+  int32_t reason; /* 0 angle_too_small, 1 interceptable, 2 clear */
+  int32_t pad;
+  double shot_angle, target_x, target_y;
+} pp_shot_decision;
+
+/* decide_shot (pass_eval.cpp:194-233) for our robot shooter_id (not on team
+ * ours -> PP_VALIDATION, as the CLI's lookup). */
+pp_status pp_decide_shot(pp_ctx* ctx, const pp_world* world, const pp_params* params,
+                         int32_t shooter_id, pp_shot_decision* out);
+
+typedef struct pp_candidate { /* PassCandidate, dpps.hpp:47-57 */
+  int32_t kick_type; /* 0 flat, 1 chip */
+  int32_t dir_index, power_index, our_id, opp_id, feasible;
+  double our_time, opp_time, receive_x, receive_y;
+} pp_candidate;
+
+typedef struct pp_free_kick_plan { /* FreeKickPlan, pass_eval.hpp:79-86 */
+  double t_ball, t_robot;
+  int32_t order; /* 0 robot_first, 1 kick_first */
+  int32_t pad;
+  double kick_delay;
+} pp_free_kick_plan;
+
+/* plan_free_kick (pass_eval.cpp:235-269), host scalar arithmetic. */
+pp_status pp_plan_free_kick(pp_ctx* ctx, const pp_world* world, const pp_params* params,
+                            int32_t kicker_id, const pp_candidate* target,
+                            pp_free_kick_plan* out);
+
 #ifdef __cplusplus
 }
 #endif

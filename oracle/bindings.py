@@ -65,6 +65,19 @@ def ref():
         lib.ref_nearest_teammate.restype = C.c_int32
         lib.ref_time_frame.argtypes = [W, Pm, G, C.c_int32, C.c_int32, C.c_int32, _dp, _dp,
                                        C.c_char_p, C.c_size_t]
+        lib.ref_intercept_all.argtypes = [W, Pm, C.POINTER(abi.Kick), C.c_double,
+                                          C.POINTER(abi.Intercept), C.c_char_p, C.c_size_t]
+        lib.ref_possession.argtypes = [W, Pm, C.POINTER(abi.PossessionReport), C.c_char_p,
+                                       C.c_size_t]
+        lib.ref_decide_shot.argtypes = [W, Pm, C.c_int32, C.POINTER(abi.ShotDecision),
+                                        C.c_char_p, C.c_size_t]
+        lib.ref_plan_free_kick.argtypes = [W, Pm, C.c_int32, C.POINTER(abi.Candidate),
+                                           C.POINTER(abi.FreeKickPlan), C.c_char_p, C.c_size_t]
+        for fn in ("ref_grid_csv", "ref_pass_heatmap_csv"):
+            getattr(lib, fn).argtypes = [W, Pm, C.c_int32, C.c_char_p, C.c_size_t]
+            getattr(lib, fn).restype = C.c_int64
+        lib.ref_run_heatmap_csv.argtypes = [W, Pm, C.c_uint32, C.c_char_p, C.c_size_t]
+        lib.ref_run_heatmap_csv.restype = C.c_int64
         lib.ref_batch.argtypes = [W, C.c_int64, Pm, G, _P(C.c_int32), C.c_int32,
                                   _P(C.c_int64), _dp, _P(C.c_int64), _dp, C.c_char_p,
                                   C.c_size_t]
@@ -90,6 +103,13 @@ def oracle():
         lib.or_runmap_count.restype = C.c_int64
         lib.or_runmap.argtypes = [W, Pm, _P(abi.RunmapRequest), _vp, C.c_int64, C.c_char_p,
                                   C.c_size_t]
+        lib.or_intercept_all.argtypes = [W, Pm, _P(abi.Kick), C.c_double, _P(abi.Intercept),
+                                         C.c_char_p, C.c_size_t]
+        lib.or_possession.argtypes = [W, Pm, _P(abi.PossessionReport), C.c_char_p, C.c_size_t]
+        lib.or_decide_shot.argtypes = [W, Pm, C.c_int32, _P(abi.ShotDecision), C.c_char_p,
+                                       C.c_size_t]
+        lib.or_plan_free_kick.argtypes = [W, Pm, C.c_int32, _P(abi.Candidate),
+                                          _P(abi.FreeKickPlan), C.c_char_p, C.c_size_t]
         lib.or_direction_table.argtypes = [C.c_int32, _dp]
         lib.or_direction_table.restype = None
         lib.or_nearest_teammate.argtypes = [W]

@@ -103,8 +103,17 @@ typedef struct {
   double ox, oy, ux, uy, speed, v1, slide, roll, t_se, d_se, t_stop, d_stop, from;
 } traj_t;
 
+/* slide_phase 0 = BallTrajectory::free_roll (ball_model.cpp:72-75) */
+static traj_t resolve_phase(double ox, double oy, double dx, double dy, double speed, int chip,
+                            const pp_ball_model* bm, int slide_phase);
+
 static traj_t resolve(double ox, double oy, double dx, double dy, double speed, int chip,
                       const pp_ball_model* bm) {
+  return resolve_phase(ox, oy, dx, dy, speed, chip, bm, 1);
+}
+
+static traj_t resolve_phase(double ox, double oy, double dx, double dy, double speed, int chip,
+                            const pp_ball_model* bm, int slide_phase) {
   traj_t t;
   memset(&t, 0, sizeof(t));
   t.ox = ox;
@@ -120,9 +129,11 @@ static traj_t resolve(double ox, double oy, double dx, double dy, double speed, 
     t.ux = dx / n;
     t.uy = dy / n;
   }
-  t.v1 = bm->transition_ratio * speed;
-  t.t_se = (speed - t.v1) / bm->slide_decel;
-  t.d_se = (speed * speed - t.v1 * t.v1) / (2.0 * bm->slide_decel);
+  t.v1 = slide_phase ? bm->transition_ratio * speed : speed;
+  if (slide_phase) {
+    t.t_se = (speed - t.v1) / bm->slide_decel;
+    t.d_se = (speed * speed - t.v1 * t.v1) / (2.0 * bm->slide_decel);
+  }
   t.t_stop = t.t_se + t.v1 / bm->roll_decel;
   t.d_stop = t.d_se + (t.v1 * t.v1) / (2.0 * bm->roll_decel);
   t.from = chip ? bm->chip_flight_fraction * t.d_stop : 0.0;
@@ -1066,5 +1077,231 @@ int or_runmap(const pp_world* w, const pp_params* p, const pp_runmap_request* re
       s->best_order[s->n_best++] = i;
     }
   }
+  return PP_OK;
+}
+
+/* ==== SURVEY §8(f): interception, possession, shot, free kick ============ */
+
+static const char* ball_error(const pp_ball_model* b) { /* ball_model.cpp:47-60 */
+  if (!(b->slide_decel > b->roll_decel) || !(b->roll_decel > 0.0))
+    return "ball model requires slide_decel > roll_decel > 0";
+  if (!(b->transition_ratio > 0.0) || !(b->transition_ratio < 1.0))
+    return "transition_ratio must lie in (0,1)";
+  if (!(b->power_min > 0.0) || !(b->power_min < b->power_max))
+    return "ball model requires 0 < power_min < power_max";
+  if (!(b->chip_flight_fraction > 0.0) || !(b->chip_flight_fraction < 1.0))
+    return "chip_flight_fraction must lie in (0,1)";
+  return NULL;
+}
+
+/* BallTrajectory::{flat_kick, chip_kick, free_roll} with resolve's checks
+ * (ball_model.cpp:12-75). */
+static int kick_traj(const pp_kick* k, const pp_ball_model* b, traj_t* out, char* msg,
+                     size_t len) {
+  const char* e = ball_error(b);
+  if (e) {
+    put(msg, len, e);
+    return PP_CONFIG;
+  }
+  const int roll = k->kind == 2;
+  const double speed = roll ? sqrt(k->dir_x * k->dir_x + k->dir_y * k->dir_y) : k->speed;
+  if (!(speed >= 0.0) || !isfinite(speed)) {
+    put(msg, len, "kick speed must be finite and non-negative");
+    return PP_DOMAIN;
+  }
+  if (sqrt(k->dir_x * k->dir_x + k->dir_y * k->dir_y) == 0.0 && speed > 0.0) {
+    put(msg, len, "kick direction must be non-zero");
+    return PP_DOMAIN;
+  }
+  *out = resolve_phase(k->origin_x, k->origin_y, k->dir_x, k->dir_y, speed, k->kind == 1, b, !roll);
+  return PP_OK;
+}
+
+/* intercept_with (intercept.cpp:121-150) */
+static pp_intercept intercept_with(const traj_t* tr, double dt, window_t win, const kin_t* kin) {
+  or_counts c;
+  memset(&c, 0, sizeof(c));
+  pp_intercept r;
+  memset(&r, 0, sizeof(r));
+  r.robot_id = kin->id;
+  const int k = scan_robot(tr, dt, win.kb, win.ke, kin, &c);
+  if (k >= 0) {
+    const double s = distance_at(tr, k * dt);
+    r.finite = 1;
+    r.time = k * dt;
+    r.point_x = tr->ox + tr->ux * s;
+    r.point_y = tr->oy + tr->uy * s;
+  } else if (win.rif) {
+    const double rx = tr->ox + tr->ux * tr->d_stop, ry = tr->oy + tr->uy * tr->d_stop;
+    const double arr = arrival_to_point(rx, ry, kin->px, kin->py, kin->vx, kin->vy, kin->a, kin->b,
+                                        kin->vmax, kin->radius);
+    r.finite = 1;
+    r.time = arr > tr->t_stop ? arr : tr->t_stop;
+    r.point_x = rx;
+    r.point_y = ry;
+  }
+  return r;
+}
+
+/* TrajectorySamples count + scan_window along the unit direction
+ * (intercept.cpp:12-25, 154-170) */
+static window_t traj_window(const traj_t* tr, const pp_field* f, double dt) {
+  const int count = (int)floor(tr->t_stop / dt + 1e-9) + 1;
+  double d_exit = 0.0;
+  const int has_exit = ray_exit(f, tr->ox, tr->oy, tr->ux, tr->uy, &d_exit);
+  return scan_window(tr, count, dt, has_exit, d_exit);
+}
+
+int or_intercept_all(const pp_world* w, const pp_params* p, const pp_kick* k, double dt,
+                     pp_intercept* out, char* msg, size_t msg_len) {
+  if (!(dt > 0.0)) {
+    put(msg, msg_len, "intercept_all: dt must be > 0");
+    return PP_DOMAIN;
+  }
+  traj_t tr;
+  const int st = kick_traj(k, &p->ball, &tr, msg, msg_len);
+  if (st != PP_OK) return st;
+  const window_t win = traj_window(&tr, &w->field, dt);
+  int n = 0;
+  for (int team = 0; team < 2; ++team) { /* intercept.cpp:176-195 */
+    const pp_robot* r = team ? w->theirs : w->ours;
+    const int nr = team ? w->n_theirs : w->n_ours;
+    int idx[PP_MAX_TEAM];
+    id_order(r, nr, idx);
+    for (int i = 0; i < nr; ++i) {
+      const kin_t kin = make_kin(&r[idx[i]], team ? &p->motion_theirs : &p->motion_ours,
+                                 p->thresholds.robot_radius);
+      out[n] = intercept_with(&tr, dt, win, &kin);
+      out[n].team = team;
+      ++n;
+    }
+  }
+  return PP_OK;
+}
+
+int or_possession(const pp_world* w, const pp_params* p, pp_possession_report* out, char* msg,
+                  size_t msg_len) {
+  const pp_kick roll = {w->ball_px, w->ball_py, w->ball_vx, w->ball_vy, 0.0, 2, 0};
+  pp_intercept all[2 * PP_MAX_TEAM];
+  const int st = or_intercept_all(w, p, &roll, p->thresholds.possession_dt, all, msg, msg_len);
+  if (st != PP_OK) return st;
+  memset(out, 0, sizeof(*out));
+  for (int i = 0; i < w->n_ours + w->n_theirs; ++i) { /* pass_eval.cpp:279-283 */
+    if (!all[i].finite) continue;
+    int32_t* has = all[i].team == 0 ? &out->has_our : &out->has_their;
+    double* t = all[i].team == 0 ? &out->our_time : &out->their_time;
+    if (!*has || all[i].time < *t) {
+      *has = 1;
+      *t = all[i].time;
+    }
+  }
+  if (!out->has_our && !out->has_their) {
+    out->side = 2;
+  } else if (!out->has_their) {
+    out->side = 0;
+  } else if (!out->has_our) {
+    out->side = 1;
+  } else {
+    const double delta = out->our_time - out->their_time;
+    out->side = fabs(delta) <= p->thresholds.contest_epsilon ? 2 : (delta < 0.0 ? 0 : 1);
+  }
+  return PP_OK;
+}
+
+int or_decide_shot(const pp_world* w, const pp_params* p, int32_t shooter_id,
+                   pp_shot_decision* out, char* msg, size_t msg_len) {
+  const pp_robot* sh = NULL;
+  for (int i = 0; i < w->n_ours; ++i)
+    if (w->ours[i].id == shooter_id) sh = &w->ours[i];
+  if (!sh) {
+    put(msg, msg_len, "kicker id not on team ours");
+    return PP_VALIDATION;
+  }
+  memset(out, 0, sizeof(*out));
+  const int has_ball = dist2(sh->px, sh->py, w->ball_px, w->ball_py) <= p->thresholds.possession_radius;
+  const double ox = has_ball ? w->ball_px : sh->px, oy = has_ball ? w->ball_py : sh->py;
+  const double r = p->thresholds.robot_radius;
+  const view_t v = goal_view(ox, oy, w, r);
+  const double gx = 0.5 * w->field.length;
+  out->shot_angle = v.angle;
+  out->target_x = gx;
+  out->target_y = v.ty;
+  if (v.angle < p->thresholds.angle_threshold || v.angle <= 0.0) {
+    out->reason = 0;
+    out->blocked = 1;
+    return PP_OK;
+  }
+  const double speed = p->thresholds.shot_power > 0.0 ? p->thresholds.shot_power : p->ball.power_max;
+  const pp_kick kick = {ox, oy, gx - ox, v.ty - oy, speed, 0, 0};
+  traj_t tr;
+  const int st = kick_traj(&kick, &p->ball, &tr, msg, msg_len);
+  if (st != PP_OK) return st;
+  double t_goal;
+  if (!travel_time(&tr, dist2(ox, oy, gx, v.ty), &t_goal)) {
+    out->reason = 1;
+    out->blocked = 1;
+    return PP_OK;
+  }
+  const double dt = p->thresholds.sbip_dt;
+  const window_t win = traj_window(&tr, &w->field, dt);
+  for (int i = 0; i < w->n_theirs; ++i) { /* world.theirs in input order */
+    const kin_t kin = make_kin(&w->theirs[i], &p->motion_theirs, r);
+    const pp_intercept ir = intercept_with(&tr, dt, win, &kin);
+    if (ir.finite && ir.time < t_goal) {
+      out->reason = 1;
+      out->blocked = 1;
+      return PP_OK;
+    }
+  }
+  out->shoot = 1;
+  out->reason = 2;
+  return PP_OK;
+}
+
+int or_plan_free_kick(const pp_world* w, const pp_params* p, int32_t kicker_id,
+                      const pp_candidate* c, pp_free_kick_plan* out, char* msg, size_t msg_len) {
+  char buf[160];
+  if (!c->feasible) {
+    put(msg, msg_len, "plan_free_kick: target candidate is not feasible");
+    return PP_DOMAIN;
+  }
+  const pp_robot* kk = NULL;
+  const pp_robot* rcv = NULL;
+  for (int i = 0; i < w->n_ours; ++i) {
+    if (w->ours[i].id == kicker_id) kk = &w->ours[i];
+    if (w->ours[i].id == c->our_id && !rcv) rcv = &w->ours[i];
+  }
+  if (!kk) {
+    snprintf(buf, sizeof(buf), "plan_free_kick: kicker id %d is not on team ours", kicker_id);
+    put(msg, msg_len, buf);
+    return PP_VALIDATION;
+  }
+  if (!rcv) {
+    snprintf(buf, sizeof(buf), "plan_free_kick: receiver id %d is not on team ours", c->our_id);
+    put(msg, msg_len, buf);
+    return PP_VALIDATION;
+  }
+  const pp_search_grid* g = &p->grid;
+  if (c->power_index < 0 || c->power_index >= g->n_powers) {
+    put(msg, msg_len, "plan_free_kick: candidate power index outside the configured grid");
+    return PP_DOMAIN;
+  }
+  const double power = power_of(c->power_index, g->n_powers, g->power_min, g->power_max);
+  const double dx = c->receive_x - w->ball_px, dy = c->receive_y - w->ball_py;
+  const pp_kick kick = {w->ball_px, w->ball_py, dx, dy, power, c->kick_type == 1 ? 1 : 0, 0};
+  traj_t tr;
+  const int st = kick_traj(&kick, &p->ball, &tr, msg, msg_len);
+  if (st != PP_OK) return st;
+  double t_ball;
+  if (!travel_time(&tr, sqrt(dx * dx + dy * dy), &t_ball)) {
+    put(msg, msg_len, "plan_free_kick: receive point beyond the ball's rollout");
+    return PP_DOMAIN;
+  }
+  memset(out, 0, sizeof(*out));
+  out->t_ball = t_ball;
+  out->t_robot = arrival_time(rcv->px, rcv->py, rcv->vx, rcv->vy, c->receive_x, c->receive_y,
+                              &p->motion_ours);
+  out->order = out->t_robot <= out->t_ball ? 1 : 0;
+  out->kick_delay = out->t_robot - out->t_ball > 0.0 ? out->t_robot - out->t_ball : 0.0;
   return PP_OK;
 }

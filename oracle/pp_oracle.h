@@ -48,6 +48,16 @@ int64_t or_runmap_count(const pp_world* w, const pp_params* p, uint32_t zone_mas
 int or_runmap(const pp_world* w, const pp_params* p, const pp_runmap_request* req, void* block,
               int64_t block_vertices, char* msg, size_t msg_len);
 
+/* intercept_all, possession, decide_shot, plan_free_kick */
+int or_intercept_all(const pp_world* w, const pp_params* p, const pp_kick* k, double dt,
+                     pp_intercept* out, char* msg, size_t msg_len);
+int or_possession(const pp_world* w, const pp_params* p, pp_possession_report* out, char* msg,
+                  size_t msg_len);
+int or_decide_shot(const pp_world* w, const pp_params* p, int32_t shooter_id,
+                   pp_shot_decision* out, char* msg, size_t msg_len);
+int or_plan_free_kick(const pp_world* w, const pp_params* p, int32_t kicker_id,
+                      const pp_candidate* c, pp_free_kick_plan* out, char* msg, size_t msg_len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,8 @@
 
 #include "oracles.hpp"
 #include "passplan/config.hpp"
+#include "passplan/csv.hpp"
+#include "passplan/intercept.hpp"
 #include "passplan/dpps.hpp"
 #include "passplan/errors.hpp"
 #include "passplan/kernels/kernel.hpp"
@@ -535,6 +537,174 @@ int ref_batch(const pp_world* frames, int64_t n_frames, const pp_params* params,
     *wall_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
     if (failed.load()) throw internal_error("a frame failed in ref_batch");
   });
+}
+
+}  // extern "C"
+
+// ---- §8(f) rows: interception, possession, shot, free kick, CSV ---------
+//   intercept_all    intercept.hpp:50-53      possession      pass_eval.hpp:104
+//   decide_shot      pass_eval.hpp:76-77      plan_free_kick  pass_eval.hpp:90-91
+//   grid_to_csv / heatmap_to_csv / run_heatmap_to_csv         csv.hpp:22-52
+namespace {
+
+BallTrajectory to_trajectory(const pp_kick& k, const BallModelParams& b) {
+  const Vec2 o{k.origin_x, k.origin_y}, d{k.dir_x, k.dir_y};
+  if (k.kind == 2) return BallTrajectory::free_roll(o, d, b);
+  if (k.kind == 1) return BallTrajectory::chip_kick(o, d, k.speed, b);
+  return BallTrajectory::flat_kick(o, d, k.speed, b);
+}
+
+PassCandidate to_candidate(const pp_candidate& c) {
+  PassCandidate p;
+  p.kick_type = c.kick_type == 1 ? KickType::chip : KickType::flat;
+  p.dir_index = c.dir_index;
+  p.power_index = c.power_index;
+  p.our_id = c.our_id;
+  p.opp_id = c.opp_id;
+  p.feasible = c.feasible != 0;
+  p.our_time = c.our_time;
+  p.opp_time = c.opp_time;
+  p.receive_point = {c.receive_x, c.receive_y};
+  return p;
+}
+
+int64_t put_text(const std::string& s, char* buf, size_t len) {
+  if (buf != nullptr && len > 0) {
+    const size_t n = s.size() < len - 1 ? s.size() : len - 1;
+    std::memcpy(buf, s.data(), n);
+    buf[n] = '\0';
+  }
+  return static_cast<int64_t>(s.size());
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_intercept_all(const pp_world* world, const pp_params* params, const pp_kick* kick,
+                      double dt, pp_intercept* out, char* msg, size_t msg_len) {
+  return guarded(msg, msg_len, [&] {
+    const WorldState w = to_world(*world);
+    const PlannerConfig cfg = to_config(*params);
+    const auto all = intercept_all(w, to_trajectory(*kick, cfg.ball), cfg.motion_ours,
+                                   cfg.motion_theirs, dt, cfg.thresholds.robot_radius);
+    for (size_t i = 0; i < all.size(); ++i) {
+      pp_intercept& o = out[i];
+      std::memset(&o, 0, sizeof(o));
+      o.team = all[i].team == Team::ours ? 0 : 1;
+      o.robot_id = all[i].robot_id;
+      o.finite = all[i].finite() ? 1 : 0;
+      if (all[i].finite()) {
+        o.time = *all[i].intercept_time;
+        o.point_x = all[i].intercept_point.x;
+        o.point_y = all[i].intercept_point.y;
+      }
+    }
+  });
+}
+
+int ref_possession(const pp_world* world, const pp_params* params, pp_possession_report* out,
+                   char* msg, size_t msg_len) {
+  return guarded(msg, msg_len, [&] {
+    const PossessionReport r = possession(to_world(*world), to_config(*params));
+    std::memset(out, 0, sizeof(*out));
+    out->side = r.side == PossessionSide::ours ? 0 : (r.side == PossessionSide::theirs ? 1 : 2);
+    out->has_our = r.our_time.has_value();
+    out->has_their = r.their_time.has_value();
+    out->our_time = r.our_time.value_or(0.0);
+    out->their_time = r.their_time.value_or(0.0);
+  });
+}
+
+int ref_decide_shot(const pp_world* world, const pp_params* params, int32_t shooter_id,
+                    pp_shot_decision* out, char* msg, size_t msg_len) {
+  return guarded(msg, msg_len, [&] {
+    const WorldState w = to_world(*world);
+    const RobotState* shooter = w.find(Team::ours, shooter_id);
+    if (shooter == nullptr) throw validation_error("kicker id not on team ours");
+    const ShotDecision d = decide_shot(*shooter, w, to_config(*params));
+    std::memset(out, 0, sizeof(*out));
+    out->shoot = d.shoot;
+    out->blocked = d.blocked;
+    out->reason = d.reason == ShotReason::angle_too_small ? 0
+                  : d.reason == ShotReason::interceptable ? 1
+                                                           : 2;
+    out->shot_angle = d.shot_angle;
+    out->target_x = d.shot_target.x;
+    out->target_y = d.shot_target.y;
+  });
+}
+
+int ref_plan_free_kick(const pp_world* world, const pp_params* params, int32_t kicker_id,
+                       const pp_candidate* target, pp_free_kick_plan* out, char* msg,
+                       size_t msg_len) {
+  return guarded(msg, msg_len, [&] {
+    const FreeKickPlan p =
+        plan_free_kick(to_world(*world), kicker_id, to_candidate(*target), to_config(*params));
+    std::memset(out, 0, sizeof(*out));
+    out->t_ball = p.t_ball;
+    out->t_robot = p.t_robot;
+    out->order = p.order == KickOrder::kick_first ? 1 : 0;
+    out->kick_delay = p.kick_delay;
+  });
+}
+
+// `passplan plan --out` CSV of one frame (passplan_main.cpp:89, csv.cpp:85-114).
+// Returns the text length (buf gets a NUL-terminated copy, truncated to len).
+int64_t ref_grid_csv(const pp_world* world, const pp_params* params, int32_t kicker_id,
+                     char* buf, size_t len) {
+  try {
+    const PlannerConfig cfg = to_config(*params);
+    const CandidateGrid g = run_dpps_serial(to_world(*world), kicker_id, cfg.grid, cfg);
+    return put_text(grid_to_csv(g), buf, len);
+  } catch (...) {
+    return -1;
+  }
+}
+
+// `passplan heatmap --mode pass` CSV (passplan_main.cpp:137-149).
+int64_t ref_pass_heatmap_csv(const pp_world* world, const pp_params* params, int32_t kicker_id,
+                             char* buf, size_t len) {
+  try {
+    const WorldState w = to_world(*world);
+    const PlannerConfig cfg = to_config(*params);
+    const CandidateGrid g = run_dpps_serial(w, kicker_id, cfg.grid, cfg);
+    std::vector<HeatPoint> pts;
+    for (const PassCandidate& c : g.cells) {
+      if (!c.feasible) continue;
+      pts.push_back({c.receive_point, score_pass(c, w, cfg).first});
+    }
+    return put_text(heatmap_to_csv(pts), buf, len);
+  } catch (...) {
+    return -1;
+  }
+}
+
+// `passplan heatmap --mode run --zone <mask>` CSV (passplan_main.cpp:156-196);
+// zone_mask bit z = ZoneLabel I..IV in that order.
+int64_t ref_run_heatmap_csv(const pp_world* world, const pp_params* params, uint32_t zone_mask,
+                            char* buf, size_t len) {
+  try {
+    const WorldState w = to_world(*world);
+    const PlannerConfig cfg = to_config(*params);
+    const ZonePartition part =
+        partition_zones(w.field, w.ball.position, cfg.thresholds.min_zone_width);
+    const ZoneLabel labels[4] = {ZoneLabel::I, ZoneLabel::II, ZoneLabel::III, ZoneLabel::IV};
+    std::vector<RunHeatRow> rows;
+    for (int z = 0; z < 4; ++z) {
+      if (!(zone_mask & (1u << z))) continue;
+      for (Vec2 v : zone_lattice(part.zone(labels[z]), cfg.thresholds.grid_step)) {
+        try {
+          const auto [score, ft] = score_running_point(v, w, cfg);
+          rows.push_back({v, ft, score});
+        } catch (const Error&) {
+        }
+      }
+    }
+    return put_text(run_heatmap_to_csv(rows), buf, len);
+  } catch (...) {
+    return -1;
+  }
 }
 
 }  // extern "C"

@@ -125,6 +125,37 @@ class RunmapRequest(C.Structure):
                 ("want_map", _I)]
 
 
+class Kick(C.Structure):  # pp_kick
+    _fields_ = [("origin_x", _D), ("origin_y", _D), ("dir_x", _D), ("dir_y", _D), ("speed", _D),
+                ("kind", _I), ("pad", _I)]
+
+
+class Intercept(C.Structure):  # pp_intercept
+    _fields_ = [("team", _I), ("robot_id", _I), ("finite", _I), ("pad", _I), ("time", _D),
+                ("point_x", _D), ("point_y", _D)]
+
+
+class PossessionReport(C.Structure):  # pp_possession_report
+    _fields_ = [("side", _I), ("has_our", _I), ("has_their", _I), ("pad", _I),
+                ("our_time", _D), ("their_time", _D)]
+
+
+class ShotDecision(C.Structure):  # pp_shot_decision
+    _fields_ = [("shoot", _I), ("blocked", _I), ("reason", _I), ("pad", _I),
+                ("shot_angle", _D), ("target_x", _D), ("target_y", _D)]
+
+
+class Candidate(C.Structure):  # pp_candidate
+    _fields_ = [("kick_type", _I), ("dir_index", _I), ("power_index", _I), ("our_id", _I),
+                ("opp_id", _I), ("feasible", _I), ("our_time", _D), ("opp_time", _D),
+                ("receive_x", _D), ("receive_y", _D)]
+
+
+class FreeKickPlan(C.Structure):  # pp_free_kick_plan
+    _fields_ = [("t_ball", _D), ("t_robot", _D), ("order", _I), ("pad", _I),
+                ("kick_delay", _D)]
+
+
 # ---------------------------------------------------------------------------
 # Result block layouts (mirror include/passplan_b200_layout.h).
 
@@ -260,9 +291,16 @@ def _declare(lib):
     lib.pp_batch_upload.argtypes = [vp, _P(World), C.c_int64, _P(C.c_int32)]
     lib.pp_batch_run.argtypes = [vp, _P(Params), _P(SearchGrid), _P(C.c_float)]
     lib.pp_batch_download.argtypes = [vp, _P(DppsSummary)]
+    lib.pp_intercept_all.argtypes = [vp, _P(World), _P(Params), _P(Kick), C.c_double,
+                                     _P(Intercept)]
+    lib.pp_possession.argtypes = [vp, _P(World), _P(Params), _P(PossessionReport)]
+    lib.pp_decide_shot.argtypes = [vp, _P(World), _P(Params), _I, _P(ShotDecision)]
+    lib.pp_plan_free_kick.argtypes = [vp, _P(World), _P(Params), _I, _P(Candidate),
+                                      _P(FreeKickPlan)]
     for fn in ("pp_params_validate", "pp_ctx_create", "pp_dpps", "pp_dpps_relaunch", "pp_score_cells",
                "pp_goal_views", "pp_runmap_count", "pp_runmap", "pp_dpps_batch",
-               "pp_batch_upload", "pp_batch_run", "pp_batch_download"):
+               "pp_batch_upload", "pp_batch_run", "pp_batch_download", "pp_intercept_all",
+               "pp_possession", "pp_decide_shot", "pp_plan_free_kick"):
         getattr(lib, fn).restype = C.c_int
     return lib
 
@@ -289,5 +327,6 @@ EXPORTED_SYMBOLS = (
     "pp_host_free", "pp_dpps", "pp_dpps_relaunch", "pp_ctx_stream", "pp_dpps_kernel_times",
     "pp_grid_cells", "pp_score_cells", "pp_goal_views", "pp_runmap",
     "pp_dpps_batch", "pp_batch_upload", "pp_batch_run", "pp_batch_download",
-    "pp_score_running_points",
+    "pp_score_running_points", "pp_intercept_all", "pp_possession", "pp_decide_shot",
+    "pp_plan_free_kick",
 )

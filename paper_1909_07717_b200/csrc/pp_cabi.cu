@@ -124,8 +124,8 @@ void put(char* msg, size_t len, const std::string& s) {
 // PlannerConfig::validate (config.cpp:172-200) minus SvgStyle, plus
 // BallModelParams/MotionLimits::validate (ball_model.cpp:47-60, motion.cpp:10-14)
 // and SearchGrid::validate (dpps.cpp:22-28).
-bool validate_params(const pp_params& p, std::string* why) {
-  const pp_ball_model& b = p.ball;
+// BallModelParams::validate (ball_model.cpp:47-60).
+bool validate_ball(const pp_ball_model& b, std::string* why) {
   if (!(b.slide_decel > b.roll_decel) || !(b.roll_decel > 0.0)) {
     *why = "ball model requires slide_decel > roll_decel > 0";
     return false;
@@ -142,6 +142,11 @@ bool validate_params(const pp_params& p, std::string* why) {
     *why = "chip_flight_fraction must lie in (0,1)";
     return false;
   }
+  return true;
+}
+
+bool validate_params(const pp_params& p, std::string* why) {
+  if (!validate_ball(p.ball, why)) return false;
   for (const pp_motion_limits* m : {&p.motion_ours, &p.motion_theirs}) {
     if (!(m->max_speed > 0.0) || !(m->max_accel > 0.0) || !(m->max_decel > 0.0)) {
       *why = "motion limits must all be positive";
@@ -248,8 +253,12 @@ std::vector<int> id_order(const pp_robot* robots, int n) {
 
 // Stages one world into FrameDev.  Returns false (validation) when the kicker
 // is not on team ours (dpps.cpp:221-223).
+// Scan list of a packed frame: the DPPS search scans ours minus the kicker
+// then theirs; interception scans everybody or the opponents only.
+enum class ScanList { kDpps, kAll, kTheirs };
+
 bool pack_frame(const pp_world& w, int32_t kicker_id, pp::FrameDev* F, int32_t* kicker_slot_out,
-                std::string* why) {
+                std::string* why, ScanList list = ScanList::kDpps) {
   std::memset(F, 0, sizeof(*F));
   if (w.n_ours < 0 || w.n_ours > PP_MAX_TEAM || w.n_theirs < 0 || w.n_theirs > PP_MAX_TEAM) {
     *why = "team size outside [0, 16]";
@@ -257,7 +266,7 @@ bool pack_frame(const pp_world& w, int32_t kicker_id, pp::FrameDev* F, int32_t* 
   }
   bool found = false;
   for (int i = 0; i < w.n_ours; ++i) found = found || w.ours[i].id == kicker_id;
-  if (!found) {
+  if (!found && list == ScanList::kDpps) {
     *why = "kicker id " + std::to_string(kicker_id) + " is not on team ours";
     return false;
   }
@@ -292,8 +301,9 @@ bool pack_frame(const pp_world& w, int32_t kicker_id, pp::FrameDev* F, int32_t* 
   F->n_theirs = w.n_theirs;
   F->kicker_slot = kicker_slot;
   int n = 0;
-  for (int s = 0; s < w.n_ours; ++s)
-    if (s != kicker_slot) F->scan_slot[n++] = static_cast<int8_t>(s);
+  if (list != ScanList::kTheirs)
+    for (int s = 0; s < w.n_ours; ++s)
+      if (s != kicker_slot || list == ScanList::kAll) F->scan_slot[n++] = static_cast<int8_t>(s);
   for (int s = 0; s < w.n_theirs; ++s) F->scan_slot[n++] = static_cast<int8_t>(pp::kTheirs + s);
   F->n_scan = n;
   *kicker_slot_out = kicker_slot;
@@ -1331,6 +1341,218 @@ pp_status pp_dpps_batch(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
                       possession_of(frames[i], k, *params));
     summaries[i].device_ms = dms;
   }
+  return PP_OK;
+}
+
+}  // extern "C"
+
+
+// ---- interception, possession, shot decision, free kick -----------------
+namespace {
+
+// BallTrajectory::resolve argument checks (ball_model.cpp:12-43).
+bool kick_path(const pp_kick& k, const pp_ball_model& b, pp::BallPath* out, pp_status* st,
+               std::string* why) {
+  if (!validate_ball(b, why)) {
+    *st = PP_CONFIG;
+    return false;
+  }
+  using pp::xd;
+  const bool roll = k.kind == 2;
+  const xd speed = roll ? pp::xsqrt(xd(k.dir_x) * xd(k.dir_x) + xd(k.dir_y) * xd(k.dir_y))
+                        : xd(k.speed);
+  if (!(speed.v >= 0.0) || !std::isfinite(speed.v)) {
+    *st = PP_DOMAIN;
+    *why = "kick speed must be finite and non-negative";
+    return false;
+  }
+  const xd n = pp::xsqrt(xd(k.dir_x) * xd(k.dir_x) + xd(k.dir_y) * xd(k.dir_y));
+  if (n.v == 0.0 && speed.v > 0.0) {
+    *st = PP_DOMAIN;
+    *why = "kick direction must be non-zero";
+    return false;
+  }
+  *out = pp::make_path(k.origin_x, k.origin_y, k.dir_x, k.dir_y, speed, k.kind == 1, !roll,
+                       b.slide_decel, b.roll_decel, b.transition_ratio, b.chip_flight_fraction);
+  return true;
+}
+
+// Runs intercept_kernel for the frame staged in ctx->frame_h (scan list set).
+cudaError_t run_intercepts(pp_ctx* ctx, const pp::FrameDev& F, const pp::DevParams& P,
+                           const pp::BallPath& B, double dt, std::vector<pp::InterceptOut>* res) {
+  cudaStream_t s = ctx->stream;
+  cudaError_t e = ctx->scratch_out.reserve(sizeof(pp::InterceptOut) * pp::kMaxRobots);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(ctx->frame.p, &F, sizeof(F), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  res->assign(static_cast<size_t>(F.n_scan), pp::InterceptOut{});
+  if (F.n_scan == 0) return cudaStreamSynchronize(s);
+  pp::intercept_kernel<<<1, 32 * F.n_scan, 0, s>>>(static_cast<const pp::FrameDev*>(ctx->frame.p),
+                                                   P, B, dt,
+                                                   static_cast<pp::InterceptOut*>(ctx->scratch_out.p));
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(res->data(), ctx->scratch_out.p, sizeof(pp::InterceptOut) * res->size(),
+                      cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);
+}
+
+const pp_robot* find_robot(const pp_robot* r, int n, int32_t id) {
+  for (int i = 0; i < n; ++i)
+    if (r[i].id == id) return &r[i];
+  return nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+pp_status pp_intercept_all(pp_ctx* ctx, const pp_world* world, const pp_params* params,
+                           const pp_kick* kick, double dt, pp_intercept* out) {
+  if (!ctx || !world || !params || !kick || !out) return fail(ctx, PP_INTERNAL, "null argument");
+  ctx->err.clear();
+  std::string why;
+  if (!(dt > 0.0)) return fail(ctx, PP_DOMAIN, "intercept_all: dt must be > 0");
+  pp::BallPath B;
+  pp_status st = PP_OK;
+  if (!kick_path(*kick, params->ball, &B, &st, &why)) return fail(ctx, st, "%s", why.c_str());
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  pp::FrameDev* F = static_cast<pp::FrameDev*>(ctx->frame_h.p);
+  int32_t ks = -1;
+  if (!pack_frame(*world, -1, F, &ks, &why, ScanList::kAll))
+    return fail(ctx, PP_VALIDATION, "%s", why.c_str());
+  const pp::DevParams P = make_dev_params(*params, params->grid);
+  std::vector<pp::InterceptOut> res;
+  PP_CUDA_TRY(ctx, run_intercepts(ctx, *F, P, B, dt, &res));
+  for (int i = 0; i < F->n_scan; ++i) {
+    const int slot = F->scan_slot[i];
+    pp_intercept& o = out[i];
+    o.team = slot >= pp::kTheirs ? 1 : 0;
+    o.robot_id = F->id[slot];
+    o.finite = res[i].finite;
+    o.pad = 0;
+    o.time = res[i].finite ? res[i].time : 0.0;
+    o.point_x = res[i].finite ? res[i].px : 0.0;
+    o.point_y = res[i].finite ? res[i].py : 0.0;
+  }
+  return PP_OK;
+}
+
+pp_status pp_possession(pp_ctx* ctx, const pp_world* world, const pp_params* params,
+                        pp_possession_report* out) {
+  if (!ctx || !world || !params || !out) return fail(ctx, PP_INTERNAL, "null argument");
+  const int n = world->n_ours + world->n_theirs;
+  if (world->n_ours < 0 || world->n_theirs < 0 || n > 2 * PP_MAX_TEAM)
+    return fail(ctx, PP_VALIDATION, "team size outside [0, 16]");
+  pp_kick roll{world->ball_px, world->ball_py, world->ball_vx, world->ball_vy, 0.0, 2, 0};
+  pp_intercept all[2 * PP_MAX_TEAM];
+  const pp_status st = pp_intercept_all(ctx, world, params, &roll,
+                                        params->thresholds.possession_dt, all);
+  if (st != PP_OK) return st;
+  std::memset(out, 0, sizeof(*out));
+  for (int i = 0; i < n; ++i) {  // fastest finite intercept per team (pass_eval.cpp:279-283)
+    if (!all[i].finite) continue;
+    int32_t* has = all[i].team == 0 ? &out->has_our : &out->has_their;
+    double* t = all[i].team == 0 ? &out->our_time : &out->their_time;
+    if (!*has || all[i].time < *t) {
+      *has = 1;
+      *t = all[i].time;
+    }
+  }
+  if (!out->has_our && !out->has_their) {
+    out->side = 2;
+  } else if (!out->has_their) {
+    out->side = 0;
+  } else if (!out->has_our) {
+    out->side = 1;
+  } else {
+    const double delta = out->our_time - out->their_time;
+    out->side = std::fabs(delta) <= params->thresholds.contest_epsilon ? 2 : (delta < 0.0 ? 0 : 1);
+  }
+  return PP_OK;
+}
+
+pp_status pp_decide_shot(pp_ctx* ctx, const pp_world* world, const pp_params* params,
+                         int32_t shooter_id, pp_shot_decision* out) {
+  if (!ctx || !world || !params || !out) return fail(ctx, PP_INTERNAL, "null argument");
+  ctx->err.clear();
+  std::string why;
+  const pp_robot* shooter = find_robot(world->ours, world->n_ours, shooter_id);
+  if (!shooter) return fail(ctx, PP_VALIDATION, "kicker id not on team ours");
+  if (!validate_ball(params->ball, &why)) return fail(ctx, PP_CONFIG, "%s", why.c_str());
+  const double shot_speed =
+      params->thresholds.shot_power > 0.0 ? params->thresholds.shot_power : params->ball.power_max;
+  if (!(shot_speed >= 0.0) || !std::isfinite(shot_speed))
+    return fail(ctx, PP_DOMAIN, "kick speed must be finite and non-negative");
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  pp::FrameDev* F = static_cast<pp::FrameDev*>(ctx->frame_h.p);
+  int32_t ks = -1;
+  if (!pack_frame(*world, shooter_id, F, &ks, &why, ScanList::kTheirs))
+    return fail(ctx, PP_VALIDATION, "%s", why.c_str());
+  // origin: the ball when the shooter has it (pass_eval.cpp:196-199)
+  const bool has_ball = host_distance(shooter->px, shooter->py, world->ball_px, world->ball_py) <=
+                        params->thresholds.possession_radius;
+  const double ox = has_ball ? world->ball_px : shooter->px;
+  const double oy = has_ball ? world->ball_py : shooter->py;
+  const pp::DevParams P = make_dev_params(*params, params->grid);
+  cudaStream_t s = ctx->stream;
+  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(sizeof(pp_shot_decision)));
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->frame.p, F, sizeof(*F), cudaMemcpyHostToDevice, s));
+  pp::shot_kernel<<<1, 32 * std::max(F->n_scan, 2), 0, s>>>(
+      static_cast<const pp::FrameDev*>(ctx->frame.p), P, ox, oy, shot_speed,
+      params->thresholds.angle_threshold, static_cast<pp_shot_decision*>(ctx->scratch_out.p));
+  PP_CUDA_TRY(ctx, cudaGetLastError());
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(out, ctx->scratch_out.p, sizeof(*out), cudaMemcpyDeviceToHost, s));
+  PP_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  return PP_OK;
+}
+
+pp_status pp_plan_free_kick(pp_ctx* ctx, const pp_world* world, const pp_params* params,
+                            int32_t kicker_id, const pp_candidate* target,
+                            pp_free_kick_plan* out) {
+  if (!ctx || !world || !params || !target || !out)
+    return fail(ctx, PP_INTERNAL, "null argument");
+  ctx->err.clear();
+  using pp::xd;
+  if (!target->feasible)
+    return fail(ctx, PP_DOMAIN, "plan_free_kick: target candidate is not feasible");
+  if (!find_robot(world->ours, world->n_ours, kicker_id))
+    return fail(ctx, PP_VALIDATION, "plan_free_kick: kicker id %d is not on team ours", kicker_id);
+  const pp_robot* rcv = find_robot(world->ours, world->n_ours, target->our_id);
+  if (!rcv)
+    return fail(ctx, PP_VALIDATION, "plan_free_kick: receiver id %d is not on team ours",
+                target->our_id);
+  const pp_search_grid& g = params->grid;
+  if (target->power_index < 0 || target->power_index >= g.n_powers)
+    return fail(ctx, PP_DOMAIN,
+                "plan_free_kick: candidate power index outside the configured grid");
+  // power_table (dpps.cpp:50-62)
+  xd power = g.power_min;
+  if (g.n_powers != 1)
+    power = xd(g.power_min) + (xd(double(target->power_index)) * (xd(g.power_max) - xd(g.power_min))) /
+                                  xd(double(g.n_powers - 1));
+  pp_kick k{world->ball_px, world->ball_py, (xd(target->receive_x) - xd(world->ball_px)).v,
+            (xd(target->receive_y) - xd(world->ball_py)).v, power.v, target->kick_type == 1 ? 1 : 0,
+            0};
+  pp::BallPath B;
+  pp_status st = PP_OK;
+  std::string why;
+  if (!kick_path(k, params->ball, &B, &st, &why)) return fail(ctx, st, "%s", why.c_str());
+  const xd dlen = pp::xsqrt(xd(k.dir_x) * xd(k.dir_x) + xd(k.dir_y) * xd(k.dir_y));
+  const xd t_ball =
+      pp::travel_time_to_distance(B.tr, params->ball.slide_decel, params->ball.roll_decel, dlen);
+  if (std::isnan(t_ball.v))
+    return fail(ctx, PP_DOMAIN, "plan_free_kick: receive point beyond the ball's rollout");
+  const pp_motion_limits& m = params->motion_ours;
+  const xd t_robot = pp::arrival_time(rcv->px, rcv->py, rcv->vx, rcv->vy, target->receive_x,
+                                      target->receive_y, m.max_accel, m.max_decel, m.max_speed);
+  out->t_ball = t_ball.v;
+  out->t_robot = t_robot.v;
+  out->order = t_robot <= t_ball ? 1 : 0;
+  out->pad = 0;
+  const xd wait = t_robot - t_ball;
+  out->kick_delay = wait.v > 0.0 ? wait.v : 0.0;  // std::max(0.0, t_robot - t_ball)
   return PP_OK;
 }
 
