@@ -229,6 +229,11 @@ struct PlannerConfig {
     return weights.norm.length_upper > 0.0 ? weights.norm.length_upper : f.length;
   }
   void validate() const;  // config_error on the first bad value (SvgStyle excluded)
+  // JSON config (config.cpp:203-241): unknown keys and wrong types are
+  // config_error; an "svg" section is accepted (pixels_per_meter > 0
+  // checked) but not stored -- the SVG renderer is not part of the drop-in.
+  static PlannerConfig from_json_text(const std::string& text);
+  static PlannerConfig load(const std::string& path);
 };
 
 // ---- search (dpps.hpp) -------------------------------------------------------
@@ -362,6 +367,109 @@ std::vector<RunningPoint> best_running_points(const WorldState& world,
                                               const std::set<ZoneLabel>& occupied,
                                               const PlannerConfig& cfg, int n_runners = 4,
                                               std::optional<Vec2> best_pass_point = std::nullopt);
+
+// ---- ball trajectory (ball_model.hpp) ------------------------------------------
+struct BallTrajectory {
+  Vec2 origin;
+  Vec2 direction;  // unit
+  double kick_speed = 0.0;
+  KickType kick_type = KickType::flat;
+  double slide_decel = 0.0, roll_decel = 0.0;
+  double v1 = 0.0, slide_end_time = 0.0, slide_end_distance = 0.0;
+  double stop_time = 0.0, stop_distance = 0.0;
+  double interceptable_from = 0.0;  // chip: airborne until this distance
+
+  static BallTrajectory flat_kick(Vec2 origin, Vec2 dir, double speed,
+                                  const BallModelParams& params);
+  static BallTrajectory chip_kick(Vec2 origin, Vec2 dir, double speed,
+                                  const BallModelParams& params);
+  static BallTrajectory free_roll(Vec2 origin, Vec2 velocity, const BallModelParams& params);
+  double speed_at(double t) const;
+  double distance_at(double t) const;
+  Vec2 position_at(double t) const { return origin + direction * distance_at(t); }
+  bool airborne_at(double t) const;
+  std::optional<double> travel_time_to_distance(double d) const;
+  std::optional<double> time_of_first_interceptable_point(double d) const;
+};
+
+struct PassPower {
+  double kick_speed = 0.0;
+  double v1 = 0.0;
+  bool clamped = false;
+};
+PassPower pass_power_for(double d, double t, const BallModelParams& params);
+
+// ---- interception (intercept.hpp) ----------------------------------------------
+struct InterceptResult {
+  Team team = Team::ours;
+  int robot_id = -1;
+  std::optional<double> intercept_time;  // nullopt = Never
+  Vec2 intercept_point;
+  bool finite() const { return intercept_time.has_value(); }
+};
+InterceptResult intercept_time(const RobotState& robot, const BallTrajectory& traj,
+                               const MotionLimits& limits, const FieldGeometry& field, double dt,
+                               double robot_radius = 0.09);
+std::vector<InterceptResult> intercept_all(const WorldState& world, const BallTrajectory& traj,
+                                           const MotionLimits& ours_limits,
+                                           const MotionLimits& theirs_limits, double dt,
+                                           double robot_radius = 0.09);
+double arrival_time(const RobotState& robot, Vec2 target, const MotionLimits& limits);
+
+// ---- shot, free kick, possession (pass_eval.hpp) --------------------------------
+enum class ShotReason { angle_too_small, interceptable, clear };
+struct ShotDecision {
+  bool shoot = false;
+  double shot_angle = 0.0;
+  Vec2 shot_target;
+  bool blocked = false;
+  ShotReason reason = ShotReason::clear;
+};
+ShotDecision decide_shot(const RobotState& shooter, const WorldState& world,
+                         const PlannerConfig& cfg);
+
+enum class KickOrder { robot_first, kick_first };
+struct FreeKickPlan {
+  double t_ball = 0.0;
+  double t_robot = 0.0;
+  KickOrder order = KickOrder::kick_first;
+  double kick_delay = 0.0;
+};
+FreeKickPlan plan_free_kick(const WorldState& world, int kicker_id, const PassCandidate& target,
+                            const PlannerConfig& cfg);
+
+enum class PossessionSide { ours, theirs, contested };
+struct PossessionReport {
+  PossessionSide side = PossessionSide::contested;
+  std::optional<double> our_time;
+  std::optional<double> their_time;
+};
+PossessionReport possession(const WorldState& world, const PlannerConfig& cfg);
+
+// ---- CSV (csv.hpp) and JSON snapshot / config I/O (snapshot.hpp, config.hpp) ------
+std::string format_double(double v);  // %.17g, +inf -> "never"
+double parse_double_field(const std::string& field);
+std::string grid_to_csv(const CandidateGrid& g);
+CandidateGrid grid_from_csv(const std::string& text);
+struct HeatPoint {
+  Vec2 point;
+  double value = 0.0;
+};
+std::string heatmap_to_csv(const std::vector<HeatPoint>& points);
+std::vector<HeatPoint> heatmap_from_csv(const std::string& text);
+struct RunHeatRow {
+  Vec2 point;
+  RunningPointFeatures features;
+  double score = 0.0;
+};
+std::string run_heatmap_to_csv(const std::vector<RunHeatRow>& rows);
+std::vector<RunHeatRow> run_heatmap_from_csv(const std::string& text);
+std::string read_text_file(const std::string& path);
+void write_text_file(const std::string& path, const std::string& text);  // atomic (tmp+rename)
+
+WorldState parse_world_snapshot(const std::string& bytes);
+WorldState load_world_snapshot(const std::string& path);
+std::string serialize_world_snapshot(const WorldState& w);
 
 // ---- batched frames (GPU extension, no reference counterpart) ---------------
 struct FrameBest {

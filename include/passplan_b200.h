@@ -313,6 +313,21 @@ typedef struct pp_kick { /* BallTrajectory::{flat_kick,chip_kick,free_roll}, bal
   int32_t pad;
 } pp_kick;
 
+typedef struct pp_trajectory { /* BallTrajectory, ball_model.hpp:27-66 */
+  double origin_x, origin_y;
+  double dir_x, dir_y; /* unit direction */
+  double kick_speed, v1, slide_decel, roll_decel;
+  double slide_end_time, slide_end_distance, stop_time, stop_distance, interceptable_from;
+  int32_t kick_type; /* 0 flat, 1 chip */
+  int32_t pad;
+} pp_trajectory;
+
+/* BallTrajectory::{flat_kick,chip_kick,free_roll} (ball_model.cpp:12-75):
+ * PP_CONFIG for an invalid ball model, PP_DOMAIN for a negative / non-finite
+ * speed or a zero direction with speed > 0.  Host only; msg may be NULL. */
+pp_status pp_kick_trajectory(const pp_kick* kick, const pp_ball_model* ball, pp_trajectory* out,
+                             char* msg, size_t msg_len);
+
 typedef struct pp_intercept { /* InterceptResult, intercept.hpp:13-20 */
   int32_t team;     /* 0 ours, 1 theirs */
   int32_t robot_id;
@@ -322,10 +337,11 @@ typedef struct pp_intercept { /* InterceptResult, intercept.hpp:13-20 */
 } pp_intercept;
 
 /* intercept_all (intercept.hpp:50-53, intercept.cpp:167-196): out[] gets
- * n_ours + n_theirs results, ours then theirs, each team in id order.
- * dt <= 0 -> PP_DOMAIN; invalid ball model -> PP_CONFIG. */
+ * n_ours + n_theirs results, ours then theirs, each team in id order; the
+ * teams' motion limits and robot_radius come from params.  dt <= 0 ->
+ * PP_DOMAIN. */
 pp_status pp_intercept_all(pp_ctx* ctx, const pp_world* world, const pp_params* params,
-                           const pp_kick* kick, double dt, pp_intercept* out);
+                           const pp_trajectory* traj, double dt, pp_intercept* out);
 
 typedef struct pp_possession_report { /* PossessionReport, pass_eval.hpp:93-99 */
   int32_t side; /* 0 ours, 1 theirs, 2 contested */

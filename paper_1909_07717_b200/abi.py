@@ -130,6 +130,13 @@ class Kick(C.Structure):  # pp_kick
                 ("kind", _I), ("pad", _I)]
 
 
+class Trajectory(C.Structure):  # pp_trajectory
+    _fields_ = [(n, _D) for n in ("origin_x", "origin_y", "dir_x", "dir_y", "kick_speed", "v1",
+                                  "slide_decel", "roll_decel", "slide_end_time",
+                                  "slide_end_distance", "stop_time", "stop_distance",
+                                  "interceptable_from")] + [("kick_type", _I), ("pad", _I)]
+
+
 class Intercept(C.Structure):  # pp_intercept
     _fields_ = [("team", _I), ("robot_id", _I), ("finite", _I), ("pad", _I), ("time", _D),
                 ("point_x", _D), ("point_y", _D)]
@@ -291,7 +298,10 @@ def _declare(lib):
     lib.pp_batch_upload.argtypes = [vp, _P(World), C.c_int64, _P(C.c_int32)]
     lib.pp_batch_run.argtypes = [vp, _P(Params), _P(SearchGrid), _P(C.c_float)]
     lib.pp_batch_download.argtypes = [vp, _P(DppsSummary)]
-    lib.pp_intercept_all.argtypes = [vp, _P(World), _P(Params), _P(Kick), C.c_double,
+    lib.pp_kick_trajectory.argtypes = [_P(Kick), _P(BallModel), _P(Trajectory), C.c_char_p,
+                                       C.c_size_t]
+    lib.pp_kick_trajectory.restype = C.c_int
+    lib.pp_intercept_all.argtypes = [vp, _P(World), _P(Params), _P(Trajectory), C.c_double,
                                      _P(Intercept)]
     lib.pp_possession.argtypes = [vp, _P(World), _P(Params), _P(PossessionReport)]
     lib.pp_decide_shot.argtypes = [vp, _P(World), _P(Params), _I, _P(ShotDecision)]
@@ -327,6 +337,6 @@ EXPORTED_SYMBOLS = (
     "pp_host_free", "pp_dpps", "pp_dpps_relaunch", "pp_ctx_stream", "pp_dpps_kernel_times",
     "pp_grid_cells", "pp_score_cells", "pp_goal_views", "pp_runmap",
     "pp_dpps_batch", "pp_batch_upload", "pp_batch_run", "pp_batch_download",
-    "pp_score_running_points", "pp_intercept_all", "pp_possession", "pp_decide_shot",
-    "pp_plan_free_kick",
+    "pp_score_running_points", "pp_kick_trajectory", "pp_intercept_all", "pp_possession",
+    "pp_decide_shot", "pp_plan_free_kick",
 )

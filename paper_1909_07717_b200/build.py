@@ -60,17 +60,40 @@ def build_product(force: bool = False, verbose_ptxas: bool = False, profile: boo
     return target
 
 
+def nlohmann_include() -> str:
+    """Header-only nlohmann/json 3.11 (the reference's JSON dependency); the
+    image ships it inside cudnn_frontend."""
+    import sysconfig
+    return os.path.join(sysconfig.get_paths()["purelib"], "include", "cudnn_frontend",
+                        "thirdparty", "nlohmann")
+
+
 def build_dropin(force: bool = False) -> str:
-    """lib/libpassplan.so: the reference's C++ API (include/passplan/) over the C-ABI."""
-    src = os.path.join(CSRC, "passplan_dropin.cpp")
+    """lib/libpassplan.so: the reference's C++ API (include/passplan/) over the
+    C-ABI, plus its CSV / JSON file formats."""
+    srcs = [os.path.join(CSRC, f) for f in ("passplan_dropin.cpp", "passplan_io.cpp")]
     hdrs = [os.path.join(ROOT, "include", "passplan", f)
             for f in os.listdir(os.path.join(ROOT, "include", "passplan"))]
-    if force or _stale(DROPIN_LIB, [src, LIB] + hdrs):
+    if force or _stale(DROPIN_LIB, srcs + [LIB] + hdrs):
         cxx = shutil.which("g++") or "g++"
         _run([cxx, "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-shared",
-              "-I", os.path.join(ROOT, "include"), "-o", DROPIN_LIB, src,
-              "-L", LIB_DIR, "-lpassplan_b200", "-Wl,-rpath,$ORIGIN"])
+              "-I", os.path.join(ROOT, "include"), "-I", nlohmann_include(), "-o", DROPIN_LIB,
+              *srcs, "-L", LIB_DIR, "-lpassplan_b200", "-Wl,-rpath,$ORIGIN"])
     return DROPIN_LIB
+
+
+CLI = os.path.join(PKG, "bin", "passplan_b200")
+
+
+def build_cli(force: bool = False) -> str:
+    """bin/passplan_b200: the reference CLI's planning commands on the drop-in."""
+    src = os.path.join(CSRC, "passplan_cli.cpp")
+    os.makedirs(os.path.dirname(CLI), exist_ok=True)
+    if force or _stale(CLI, [src, DROPIN_LIB]):
+        _run([shutil.which("g++") or "g++", "-std=c++20", "-O2", "-ffp-contract=off",
+              "-I", os.path.join(ROOT, "include"), src, "-o", CLI, "-L", LIB_DIR, "-lpassplan",
+              "-lpassplan_b200", "-Wl,-rpath,$ORIGIN/../lib"])
+    return CLI
 
 
 CPP_TEST = os.path.join(ROOT, "tests", "cpp", "build", "test_dropin")
@@ -104,6 +127,7 @@ def build_checkers() -> None:
 def build_all(force: bool = False) -> None:
     build_product(force=force)
     build_dropin(force=force)
+    build_cli(force=force)
     build_checkers()
     build_cpp_tests(force=force)
 

@@ -566,4 +566,273 @@ std::vector<FrameBest> best_pass_batch(const std::vector<WorldState>& frames,
   return out;
 }
 
+// ---- ball trajectory (ball_model.cpp:12-146), host ------------------------------
+namespace {
+
+BallTrajectory resolve_trajectory(Vec2 origin, Vec2 dir, double speed, KickType type,
+                                  const BallModelParams& params, bool slide_phase) {
+  params.validate();
+  if (!(speed >= 0.0) || !std::isfinite(speed))
+    throw domain_error("kick speed must be finite and non-negative");
+  BallTrajectory t;
+  t.origin = origin;
+  t.kick_speed = speed;
+  t.kick_type = type;
+  t.slide_decel = params.slide_decel;
+  t.roll_decel = params.roll_decel;
+  const double n = dir.norm();
+  if (n == 0.0) {
+    if (speed > 0.0) throw domain_error("kick direction must be non-zero");
+    t.direction = {1.0, 0.0};
+  } else {
+    t.direction = {dir.x / n, dir.y / n};
+  }
+  t.v1 = slide_phase ? params.transition_ratio * speed : speed;
+  if (slide_phase) {
+    t.slide_end_time = (speed - t.v1) / params.slide_decel;
+    t.slide_end_distance = (speed * speed - t.v1 * t.v1) / (2.0 * params.slide_decel);
+  }
+  t.stop_time = t.slide_end_time + t.v1 / params.roll_decel;
+  t.stop_distance = t.slide_end_distance + (t.v1 * t.v1) / (2.0 * params.roll_decel);
+  t.interceptable_from =
+      type == KickType::chip ? params.chip_flight_fraction * t.stop_distance : 0.0;
+  return t;
+}
+
+pp_trajectory to_pp(const BallTrajectory& t) {
+  pp_trajectory o;
+  std::memset(&o, 0, sizeof(o));
+  o.origin_x = t.origin.x;
+  o.origin_y = t.origin.y;
+  o.dir_x = t.direction.x;
+  o.dir_y = t.direction.y;
+  o.kick_speed = t.kick_speed;
+  o.v1 = t.v1;
+  o.slide_decel = t.slide_decel;
+  o.roll_decel = t.roll_decel;
+  o.slide_end_time = t.slide_end_time;
+  o.slide_end_distance = t.slide_end_distance;
+  o.stop_time = t.stop_time;
+  o.stop_distance = t.stop_distance;
+  o.interceptable_from = t.interceptable_from;
+  o.kick_type = t.kick_type == KickType::chip ? 1 : 0;
+  return o;
+}
+
+InterceptResult from_pp(const pp_intercept& r) {
+  InterceptResult o;
+  o.team = r.team == 0 ? Team::ours : Team::theirs;
+  o.robot_id = r.robot_id;
+  if (r.finite) {
+    o.intercept_time = r.time;
+    o.intercept_point = {r.point_x, r.point_y};
+  }
+  return o;
+}
+
+}  // namespace
+
+BallTrajectory BallTrajectory::flat_kick(Vec2 origin, Vec2 dir, double speed,
+                                         const BallModelParams& params) {
+  return resolve_trajectory(origin, dir, speed, KickType::flat, params, true);
+}
+
+BallTrajectory BallTrajectory::chip_kick(Vec2 origin, Vec2 dir, double speed,
+                                         const BallModelParams& params) {
+  return resolve_trajectory(origin, dir, speed, KickType::chip, params, true);
+}
+
+BallTrajectory BallTrajectory::free_roll(Vec2 origin, Vec2 velocity,
+                                         const BallModelParams& params) {
+  return resolve_trajectory(origin, velocity, velocity.norm(), KickType::flat, params, false);
+}
+
+double BallTrajectory::speed_at(double t) const {
+  if (t < slide_end_time) return kick_speed - slide_decel * t;
+  if (t < stop_time) return v1 - roll_decel * (t - slide_end_time);
+  return 0.0;
+}
+
+double BallTrajectory::distance_at(double t) const {
+  if (t < slide_end_time) return kick_speed * t - 0.5 * slide_decel * t * t;
+  if (t < stop_time) {
+    const double u = t - slide_end_time;
+    return slide_end_distance + v1 * u - 0.5 * roll_decel * u * u;
+  }
+  return stop_distance;
+}
+
+bool BallTrajectory::airborne_at(double t) const {
+  return kick_type == KickType::chip && distance_at(t) < interceptable_from;
+}
+
+std::optional<double> BallTrajectory::travel_time_to_distance(double d) const {
+  if (d == 0.0) return 0.0;
+  if (d > stop_distance) return std::nullopt;
+  if (d <= slide_end_distance) {  // stable root of d = v0 t - a t^2 / 2
+    const double rad = kick_speed * kick_speed - 2.0 * slide_decel * d;
+    return 2.0 * d / (kick_speed + std::sqrt(rad < 0.0 ? 0.0 : rad));
+  }
+  const double rem = d - slide_end_distance;
+  const double rad = v1 * v1 - 2.0 * roll_decel * rem;
+  return slide_end_time + 2.0 * rem / (v1 + std::sqrt(rad < 0.0 ? 0.0 : rad));
+}
+
+std::optional<double> BallTrajectory::time_of_first_interceptable_point(double d) const {
+  if (kick_type == KickType::chip && d < interceptable_from) return std::nullopt;
+  return travel_time_to_distance(d);
+}
+
+PassPower pass_power_for(double d, double t, const BallModelParams& params) {
+  params.validate();  // ball_model.cpp:129-146
+  if (!(d > 0.0) || !std::isfinite(d)) throw domain_error("pass_power_for: d must be > 0");
+  if (!(t > 0.0) || !std::isfinite(t)) throw domain_error("pass_power_for: t must be > 0");
+  PassPower p;
+  p.v1 = d / t + 0.5 * params.roll_decel * t;
+  p.kick_speed = p.v1 / params.transition_ratio;
+  if (p.kick_speed < params.power_min) {
+    p.kick_speed = params.power_min;
+    p.clamped = true;
+  } else if (p.kick_speed > params.power_max) {
+    p.kick_speed = params.power_max;
+    p.clamped = true;
+  }
+  return p;
+}
+
+double arrival_time(const RobotState& robot, Vec2 target, const MotionLimits& limits) {
+  // motion.cpp:16-29 with detail/arrival_math.hpp:15-69 (radius 0)
+  const double qx = target.x - robot.position.x, qy = target.y - robot.position.y;
+  const double d2 = qx * qx + qy * qy;
+  const double a = limits.max_accel, b = limits.max_decel, vmax = limits.max_speed;
+  auto rest_to_rest = [&](double L) {
+    const double peak = std::sqrt((2.0 * a) * b * L / (a + b));
+    if (peak <= vmax) return peak / a + peak / b;
+    const double d_used = (vmax * vmax) / (2.0 * a) + (vmax * vmax) / (2.0 * b);
+    return vmax / a + vmax / b + (L - d_used) / vmax;
+  };
+  auto one_d = [&](double v0, double dist) {
+    const double brake = (v0 * v0) / (2.0 * b);
+    if (v0 < 0.0 || brake > dist) {
+      const double gap = brake - std::copysign(dist, v0);
+      return std::fabs(v0) / b + rest_to_rest(gap);
+    }
+    const double peak = std::sqrt(((2.0 * a) * b * dist + b * (v0 * v0)) / (a + b));
+    if (peak <= vmax) return (peak - v0) / a + peak / b;
+    if (v0 <= vmax) {
+      const double d_used = (vmax * vmax - v0 * v0) / (2.0 * a) + (vmax * vmax) / (2.0 * b);
+      return (vmax - v0) / a + vmax / b + (dist - d_used) / vmax;
+    }
+    const double d_used = (v0 * v0 - vmax * vmax) / (2.0 * b) + (vmax * vmax) / (2.0 * b);
+    return (v0 - vmax) / b + vmax / b + (dist - d_used) / vmax;
+  };
+  if (d2 <= 1e-24) return one_d(robot.velocity.norm(), 0.0);
+  const double d = std::sqrt(d2);
+  const double denom = d > 1e-30 ? d : 1e-30;
+  const double ex = qx / denom, ey = qy / denom;
+  const double va = robot.velocity.x * ex + robot.velocity.y * ey;
+  const double vc = robot.velocity.x * ey - robot.velocity.y * ex;
+  const double t_along = one_d(va, d > 0.0 ? d : 0.0);
+  const double t_cross = std::fabs(vc) / b;
+  return t_along > t_cross ? t_along : t_cross;
+}
+
+// ---- interception, possession, shot, free kick (GPU via the C-ABI) ---------------
+
+std::vector<InterceptResult> intercept_all(const WorldState& world, const BallTrajectory& traj,
+                                           const MotionLimits& ours_limits,
+                                           const MotionLimits& theirs_limits, double dt,
+                                           double robot_radius) {
+  if (!(dt > 0.0)) throw domain_error("intercept_all: dt must be > 0");
+  pp_ctx* ctx = context();
+  const pp_world w = to_pp(world);
+  PlannerConfig cfg;
+  cfg.motion_ours = ours_limits;
+  cfg.motion_theirs = theirs_limits;
+  cfg.thresholds.robot_radius = robot_radius;
+  const pp_params p = to_pp(cfg);
+  const pp_trajectory t = to_pp(traj);
+  pp_intercept res[2 * PP_MAX_TEAM];
+  check(pp_intercept_all(ctx, &w, &p, &t, dt, res), ctx);
+  std::vector<InterceptResult> out;
+  for (int i = 0; i < w.n_ours + w.n_theirs; ++i) out.push_back(from_pp(res[i]));
+  return out;
+}
+
+InterceptResult intercept_time(const RobotState& robot, const BallTrajectory& traj,
+                               const MotionLimits& limits, const FieldGeometry& field, double dt,
+                               double robot_radius) {
+  if (!(dt > 0.0)) throw domain_error("intercept_time: dt must be > 0");
+  WorldState one;
+  one.field = field;
+  one.ours = {robot};
+  const std::vector<InterceptResult> r =
+      intercept_all(one, traj, limits, limits, dt, robot_radius);
+  InterceptResult o = r.front();
+  o.team = Team::ours;  // the reference leaves team at its default here
+  return o;
+}
+
+PossessionReport possession(const WorldState& world, const PlannerConfig& cfg) {
+  pp_ctx* ctx = context();
+  const pp_world w = to_pp(world);
+  const pp_params p = to_pp(cfg);
+  pp_possession_report r;
+  check(pp_possession(ctx, &w, &p, &r), ctx);
+  PossessionReport o;
+  o.side = r.side == 0 ? PossessionSide::ours
+                       : (r.side == 1 ? PossessionSide::theirs : PossessionSide::contested);
+  if (r.has_our) o.our_time = r.our_time;
+  if (r.has_their) o.their_time = r.their_time;
+  return o;
+}
+
+ShotDecision decide_shot(const RobotState& shooter, const WorldState& world,
+                         const PlannerConfig& cfg) {
+  // Only the shooter's position and the opponents enter (pass_eval.cpp:194-233):
+  // hand the C-ABI a world whose one teammate is the shooter.
+  WorldState w2 = world;
+  w2.ours = {shooter};
+  pp_ctx* ctx = context();
+  const pp_world w = to_pp(w2);
+  const pp_params p = to_pp(cfg);
+  pp_shot_decision d;
+  check(pp_decide_shot(ctx, &w, &p, shooter.id, &d), ctx);
+  ShotDecision o;
+  o.shoot = d.shoot != 0;
+  o.blocked = d.blocked != 0;
+  o.shot_angle = d.shot_angle;
+  o.shot_target = {d.target_x, d.target_y};
+  o.reason = d.reason == 0 ? ShotReason::angle_too_small
+                           : (d.reason == 1 ? ShotReason::interceptable : ShotReason::clear);
+  return o;
+}
+
+FreeKickPlan plan_free_kick(const WorldState& world, int kicker_id, const PassCandidate& target,
+                            const PlannerConfig& cfg) {
+  pp_ctx* ctx = context();
+  const pp_world w = to_pp(world);
+  const pp_params p = to_pp(cfg);
+  pp_candidate c;
+  std::memset(&c, 0, sizeof(c));
+  c.kick_type = target.kick_type == KickType::chip ? 1 : 0;
+  c.dir_index = target.dir_index;
+  c.power_index = target.power_index;
+  c.our_id = target.our_id;
+  c.opp_id = target.opp_id;
+  c.feasible = target.feasible ? 1 : 0;
+  c.our_time = target.our_time;
+  c.opp_time = target.opp_time;
+  c.receive_x = target.receive_point.x;
+  c.receive_y = target.receive_point.y;
+  pp_free_kick_plan fk;
+  check(pp_plan_free_kick(ctx, &w, &p, kicker_id, &c, &fk), ctx);
+  FreeKickPlan o;
+  o.t_ball = fk.t_ball;
+  o.t_robot = fk.t_robot;
+  o.order = fk.order == 1 ? KickOrder::kick_first : KickOrder::robot_first;
+  o.kick_delay = fk.kick_delay;
+  return o;
+}
+
 }  // namespace passplan

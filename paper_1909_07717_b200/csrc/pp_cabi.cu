@@ -1377,6 +1377,24 @@ bool kick_path(const pp_kick& k, const pp_ball_model& b, pp::BallPath* out, pp_s
   return true;
 }
 
+pp::BallPath path_of(const pp_trajectory& t) {
+  pp::BallPath b;
+  b.ox = t.origin_x;
+  b.oy = t.origin_y;
+  b.ux = t.dir_x;
+  b.uy = t.dir_y;
+  b.slide = t.slide_decel;
+  b.roll = t.roll_decel;
+  b.tr.speed = t.kick_speed;
+  b.tr.v1 = t.v1;
+  b.tr.t_se = t.slide_end_time;
+  b.tr.d_se = t.slide_end_distance;
+  b.tr.t_stop = t.stop_time;
+  b.tr.d_stop = t.stop_distance;
+  b.tr.from = t.interceptable_from;
+  return b;
+}
+
 // Runs intercept_kernel for the frame staged in ctx->frame_h (scan list set).
 cudaError_t run_intercepts(pp_ctx* ctx, const pp::FrameDev& F, const pp::DevParams& P,
                            const pp::BallPath& B, double dt, std::vector<pp::InterceptOut>* res) {
@@ -1408,15 +1426,44 @@ const pp_robot* find_robot(const pp_robot* r, int n, int32_t id) {
 
 extern "C" {
 
+pp_status pp_kick_trajectory(const pp_kick* kick, const pp_ball_model* ball, pp_trajectory* out,
+                             char* msg, size_t msg_len) {
+  if (!kick || !ball || !out) {
+    put(msg, msg_len, "null argument");
+    return PP_INTERNAL;
+  }
+  pp::BallPath B;
+  pp_status st = PP_OK;
+  std::string why;
+  if (!kick_path(*kick, *ball, &B, &st, &why)) {
+    put(msg, msg_len, why);
+    return st;
+  }
+  std::memset(out, 0, sizeof(*out));
+  out->origin_x = B.ox;
+  out->origin_y = B.oy;
+  out->dir_x = B.ux;
+  out->dir_y = B.uy;
+  out->kick_speed = B.tr.speed.v;
+  out->v1 = B.tr.v1.v;
+  out->slide_decel = B.slide;
+  out->roll_decel = B.roll;
+  out->slide_end_time = B.tr.t_se.v;
+  out->slide_end_distance = B.tr.d_se.v;
+  out->stop_time = B.tr.t_stop.v;
+  out->stop_distance = B.tr.d_stop.v;
+  out->interceptable_from = B.tr.from.v;
+  out->kick_type = kick->kind == 1 ? 1 : 0;
+  return PP_OK;
+}
+
 pp_status pp_intercept_all(pp_ctx* ctx, const pp_world* world, const pp_params* params,
-                           const pp_kick* kick, double dt, pp_intercept* out) {
-  if (!ctx || !world || !params || !kick || !out) return fail(ctx, PP_INTERNAL, "null argument");
+                           const pp_trajectory* traj, double dt, pp_intercept* out) {
+  if (!ctx || !world || !params || !traj || !out) return fail(ctx, PP_INTERNAL, "null argument");
   ctx->err.clear();
   std::string why;
   if (!(dt > 0.0)) return fail(ctx, PP_DOMAIN, "intercept_all: dt must be > 0");
-  pp::BallPath B;
-  pp_status st = PP_OK;
-  if (!kick_path(*kick, params->ball, &B, &st, &why)) return fail(ctx, st, "%s", why.c_str());
+  const pp::BallPath B = path_of(*traj);
   PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   pp::FrameDev* F = static_cast<pp::FrameDev*>(ctx->frame_h.p);
   int32_t ks = -1;
@@ -1445,10 +1492,13 @@ pp_status pp_possession(pp_ctx* ctx, const pp_world* world, const pp_params* par
   const int n = world->n_ours + world->n_theirs;
   if (world->n_ours < 0 || world->n_theirs < 0 || n > 2 * PP_MAX_TEAM)
     return fail(ctx, PP_VALIDATION, "team size outside [0, 16]");
-  pp_kick roll{world->ball_px, world->ball_py, world->ball_vx, world->ball_vy, 0.0, 2, 0};
+  const pp_kick roll{world->ball_px, world->ball_py, world->ball_vx, world->ball_vy, 0.0, 2, 0};
+  pp_trajectory traj;
+  char msg[256];
+  pp_status st = pp_kick_trajectory(&roll, &params->ball, &traj, msg, sizeof(msg));
+  if (st != PP_OK) return fail(ctx, st, "%s", msg);
   pp_intercept all[2 * PP_MAX_TEAM];
-  const pp_status st = pp_intercept_all(ctx, world, params, &roll,
-                                        params->thresholds.possession_dt, all);
+  st = pp_intercept_all(ctx, world, params, &traj, params->thresholds.possession_dt, all);
   if (st != PP_OK) return st;
   std::memset(out, 0, sizeof(*out));
   for (int i = 0; i < n; ++i) {  // fastest finite intercept per team (pass_eval.cpp:279-283)

@@ -156,5 +156,11 @@ def test_cpp_dropin_exports_reference_api():
                 "passplan::zone_lattice(", "passplan::partition_zones(",
                 "passplan::direction_table(", "passplan::power_table(",
                 "passplan::grids_identical(", "passplan::feasible_candidates(",
-                "passplan::PlannerConfig::validate() const", "passplan::best_pass_batch("):
+                "passplan::PlannerConfig::validate() const", "passplan::best_pass_batch(",
+                "passplan::decide_shot(", "passplan::possession(", "passplan::intercept_all(",
+                "passplan::intercept_time(", "passplan::plan_free_kick(",
+                "passplan::pass_power_for(", "passplan::BallTrajectory::flat_kick(",
+                "passplan::grid_to_csv", "passplan::grid_from_csv(", "passplan::heatmap_to_csv",
+                "passplan::run_heatmap_to_csv", "passplan::load_world_snapshot(",
+                "passplan::PlannerConfig::load("):
         assert sym in out, sym

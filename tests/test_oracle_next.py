@@ -46,3 +46,21 @@ def test_oracle_plan_free_kick():
                                      512) == st, (cid, m.value)
         if st == 0:
             assert not same(got, want), (cid, same(got, want))
+
+
+def test_kick_trajectory_status_cpu():
+    """pp_kick_trajectory is host code: its argument checks match the
+    reference's BallTrajectory::resolve (ball_model.cpp:12-43) without a GPU."""
+    lib = abi.load_library()
+    n = 0
+    for cid, w, p, k, dt, st, want in intercept_cases():
+        tr = abi.Trajectory()
+        s1 = lib.pp_kick_trajectory(C.byref(k), C.byref(p.ball), C.byref(tr), None, 0)
+        if cid in ("err_ball", "err_dir", "err_speed"):
+            assert s1 == st != 0, cid
+            n += 1
+        else:
+            assert s1 == 0, cid
+            if k.kind == 2:  # free roll: no slide phase (ball_model.cpp:72-75)
+                assert tr.slide_end_time == 0.0 and tr.v1 == tr.kick_speed
+    assert n == 3
