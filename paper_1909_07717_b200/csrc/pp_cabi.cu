@@ -367,6 +367,8 @@ pp::DevParams make_dev_params(const pp_params& p, const pp_search_grid& g) {
   d.ang_upper = p.norm.angle_upper;
   d.power_min = g.power_min;
   d.power_max = g.power_max;
+  d.dtf = static_cast<float>(d.dt);
+  d.radf = static_cast<float>(d.radius);
   d.n_dirs = g.n_directions;
   d.n_pows = g.n_powers;
   d.n_kt = (g.flat ? 1 : 0) + (g.chip ? 1 : 0);
