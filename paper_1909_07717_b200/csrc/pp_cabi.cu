@@ -531,6 +531,7 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   const pp::CellQueue q = make_queue(ctx, P, n_frames);
   auto* fc = static_cast<pp::FrameCounters*>(ctx->fcount.p);
   const int64_t chunks = chunks_for(P);
+  auto* parts = static_cast<pp::Partial*>(ctx->partials.p);
   if (ctas >= 2 * 148 * pp::kScanCtasNarrow) {
     // Throughput (>= 2 waves of the narrow shape): 4-warp CTAs, 8 per SM,
     // robots round-robin over the warps.
@@ -538,6 +539,7 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
     pp::scan_kernel<kCells, pp::kScanWarpsNarrow, pp::kScanCtasNarrow>
         <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, P, co, q, fc);
   } else {
+    // Latency: 16-warp CTAs, one robot per warp.
     const int w = n_scan < pp::kScanWarpsWide ? n_scan : pp::kScanWarpsWide;
     pp::scan_kernel<kCells, pp::kScanWarpsWide, pp::kScanCtasWide>
         <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, P, co, q, fc);
@@ -548,7 +550,6 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   // Few chunks (one frame): wider CTAs shorten each chunk's chain of
   // dependent items; many chunks: narrower CTAs pack the SMs better.
   const unsigned vctas = static_cast<unsigned>(n_frames * chunks);
-  auto* parts = static_cast<pp::Partial*>(ctx->partials.p);
   // Programmatic dependent launch: the value grid is launched while the scan
   // grid drains and waits on it in-kernel (griddepcontrol.wait).
   cudaLaunchAttribute attr[1];
@@ -563,13 +564,14 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   const int nch = static_cast<int>(chunks);
   if (vctas <= 4u * 148u) {
     cfg.blockDim = dim3(pp::kValueThreadsWide);
-    return cudaLaunchKernelEx(&cfg, pp::value_kernel<kCells, pp::kValueThreadsWide>, frames, P, q,
-                              fc, co, parts, sums, nch);
+    return cudaLaunchKernelEx(&cfg, pp::value_kernel<kCells, pp::kValueThreadsWide>, frames, P,
+                              q, fc, co, parts, sums, nch);
   }
   cfg.blockDim = dim3(pp::kValueThreads);
   return cudaLaunchKernelEx(&cfg, pp::value_kernel<kCells, pp::kValueThreads>, frames, P, q, fc,
                             co, parts, sums, nch);
 }
+
 
 // The single-frame launch of the last pp_dpps call.
 cudaError_t launch_single(pp_ctx* ctx, cudaEvent_t mid = nullptr) {

@@ -55,6 +55,10 @@ def report(label, n_scan, n_value, n_robots):
               f"{(v[:, 7].max() - t0) / 1e3:.1f} us (gap after scan "
               f"{(v[:, 0].min() - s[:, 7].max()) / 1e3:.1f} us); CTA us {pct((v[:, 7] - v[:, 0]) / 1e3)}")
         print(f"   D1 {pct(v[:, 1])}\n   D2 {pct(v[:, 2])}\n   D3 {pct(v[:, 3])}\n   red {pct(v[:, 4])}")
+        late = np.argsort(v[:, 7])[-5:]
+        for i in late:
+            print(f"   late CTA: start {(v[i, 0] - t0) / 1e3:.1f} end {(v[i, 7] - t0) / 1e3:.1f} us "
+                  f"D1 {v[i, 1]} D2 {v[i, 2]} D3 {v[i, 3]} red {v[i, 4]}")
 
 
 w, p, grid, k, _ = case_inputs(g, "f8")

@@ -1,0 +1,86 @@
+// Dev tool: D2 (goal-view edge bisection) latency per warp with 32 active
+// lanes of distinct blocking geometry: interval_edge (one divergent loop) vs
+// interval_edge_split (cheap steps, then exact rounds).  Checks both give
+// identical edges.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -o tools/edge_bench2 tools/edge_bench2.cu
+#include <cstdio>
+#include "../paper_1909_07717_b200/csrc/pp_kernels.cuh"
+
+using namespace pp;
+
+template <int kMode, int kLanes>
+__global__ void k(const FrameDev* F_, double r_lt2, double mb_le2, long long* cyc, double* out) {
+  __shared__ FrameDev F;
+  __shared__ double hts[kMaxHeights];
+  __shared__ PairInfo pis[32];
+  load_frame(&F, F_);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const ViewCtx V0 = make_view_ctx(0.0, 0.0, F, 0.09, r_lt2, mb_le2);
+  for (int i = threadIdx.x; i < V0.nh; i += blockDim.x) hts[i] = view_height(i, V0.n_half, V0.gh).v;
+  __syncthreads();
+  const double t = lane + 32.0 * blockIdx.x;
+  auto h = [&](double k) { const double x = sin(t * 12.9898 + k * 78.233) * 43758.5453; return x - floor(x); };
+  const xd px = -2.0 + 5.0 * h(1), py = -2.0 + 4.0 * h(2);
+  const double gy = -0.8 + 1.6 * h(3), f = 0.3 + 0.5 * h(4), off = (h(5) - 0.5) * 0.1;
+  const xd cx = px.v + f * (6.0 - px.v), cy = py.v + f * (gy - py.v) + off;
+  const ViewCtx V = make_view_ctx(px, py, F, 0.09, r_lt2, mb_le2, hts);
+  pis[lane] = pair_info(V, cx, cy);
+  __syncwarp();
+  const PairInfo pi = pis[lane];
+  const bool active = pi.status == 1 && lane < kLanes;
+  __syncwarp();
+  const long long t0 = clock64();
+  double acc = 0.0;
+  for (int edge = 0; edge < 2; ++edge) {
+    xd y;
+    if (kMode == 0) {
+      y = active ? interval_edge(V, cx, cy, edge, pi.first, pi.last, pi.fast, pi.y1, pi.y2,
+                                 pi.margin)
+                 : xd(0.0);
+    } else {
+      y = active ? interval_edge_split(V, cx, cy, edge, pi.first, pi.last, pi.fast, pi.y1, pi.y2,
+                                       pi.margin)
+                 : xd(0.0);
+    }
+    acc += y.v;
+  }
+  __syncwarp();
+  const long long t1 = clock64();
+  out[blockIdx.x * 32 + lane] = active ? acc : -999.0;
+  if (lane == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+int main() {
+  FrameDev F{};
+  F.L = 12.0; F.W = 9.0; F.gw = 1.8;
+  FrameDev* dF;
+  cudaMalloc(&dF, sizeof(F));
+  cudaMemcpy(dF, &F, sizeof(F), cudaMemcpyHostToDevice);
+  const double r = 0.09, r_lt2 = r * r, mb_le2 = (r + 1e-9) * (r + 1e-9);
+  long long* cyc; double* out;
+  const int nb = 64;
+  cudaMalloc(&cyc, nb * 8); cudaMalloc(&out, nb * 32 * 8);
+  double ho[6][nb * 32]; long long hc[nb];
+  for (int mode = 0; mode < 6; ++mode) {
+    for (int rep = 0; rep < 2; ++rep) {
+      if (mode == 0) k<0, 32><<<nb, 32>>>(dF, r_lt2, mb_le2, cyc, out);
+      else if (mode == 1) k<1, 32><<<nb, 32>>>(dF, r_lt2, mb_le2, cyc, out);
+      else if (mode == 2) k<0, 1><<<nb, 32>>>(dF, r_lt2, mb_le2, cyc, out);
+      else if (mode == 3) k<1, 1><<<nb, 32>>>(dF, r_lt2, mb_le2, cyc, out);
+      else if (mode == 4) k<0, 8><<<nb, 32>>>(dF, r_lt2, mb_le2, cyc, out);
+      else k<1, 8><<<nb, 32>>>(dF, r_lt2, mb_le2, cyc, out);
+    }
+    cudaDeviceSynchronize();
+    cudaMemcpy(hc, cyc, sizeof(hc), cudaMemcpyDeviceToHost);
+    cudaMemcpy(ho[mode], out, sizeof(ho[0]), cudaMemcpyDeviceToHost);
+    double s = 0; long long mx = 0; int act = 0;
+    for (int i = 0; i < nb; ++i) { s += hc[i]; mx = hc[i] > mx ? hc[i] : mx; }
+    for (int i = 0; i < nb * 32; ++i) act += ho[mode][i] != -999.0;
+    printf("mode %d: active lanes %d/%d, warp cycles mean %.0f max %lld\n", mode, act, nb * 32, s / nb, mx);
+  }
+  int diff = 0;
+  for (int i = 0; i < nb * 32; ++i) diff += ho[0][i] != ho[1][i];
+  printf("mismatches %d; %s\n", diff, cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
