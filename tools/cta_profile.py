@@ -100,18 +100,11 @@ for i in top:
 print("per robot mean cycles:", np.round(R.mean(0)).astype(int).tolist())
 print("per robot mean maxsteps:", np.round(it.max(-1).mean(0), 1).tolist())
 
-# goal-view edge bisections of one more chip=1 frame
-lib.pp_debug_edges.argtypes = [C.POINTER(C.c_int), C.POINTER(C.c_uint), C.c_int]
-E = np.zeros((1 << 15, 4), np.int32)
-ne = C.c_uint()
-lib.pp_debug_edges(E.ctypes.data_as(C.POINTER(C.c_int)), C.byref(ne), 1)
+# per-tile durations of the chip=1 frame for cost-model fitting (tools/tile_cost.py)
 grid.chip = 1
-blk = abi.GridBlock(128 * 64 * 2)
-lib.pp_dpps(ctx, C.byref(w), C.byref(p), C.byref(grid), k, 1, blk.ptr())
-lib.pp_debug_edges(E.ctypes.data_as(C.POINTER(C.c_int)), C.byref(ne), 1)
-E = E[:ne.value]
-print(f"edges {len(E)}: fast {E[:, 0].mean():.2f} iters {pct(E[:, 1])} exact {pct(E[:, 2])} cyc {pct(E[:, 3])}")
-for fl in (0, 1):
-    m = E[:, 0] == fl
-    if m.any():
-        print(f"  fast={fl}: n={m.sum()} iters {pct(E[m, 1])} exact {pct(E[m, 2])} cyc {pct(E[m, 3])}")
+blk = abi.GridBlock(16384)
+for _ in range(3):
+    lib.pp_dpps(ctx, C.byref(w), C.byref(p), C.byref(grid), k, 1, blk.ptr())
+s_, v_, r_ = records()
+np.save(os.path.join(ROOT, "gpurun_out", "tile_cycles.npy"), r_[:512, :15])
+np.save(os.path.join(ROOT, "gpurun_out", "tile_dur.npy"), (s_[:512, 7] - s_[:512, 0]))
