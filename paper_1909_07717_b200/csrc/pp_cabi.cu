@@ -376,6 +376,10 @@ pp::DevParams make_dev_params(const pp_params& p, const pp_search_grid& g) {
   d.kt_chip1 = 1;
   d.n_ptiles = (g.n_powers + 31) / 32;
   d.n_tiles = d.n_kt * g.n_directions * d.n_ptiles;
+  d.scan_steps_w = 6;
+  d.scan_steps_n = 1 << 30;
+  if (const char* e = getenv("PP_SCAN_STEPS_W")) d.scan_steps_w = atoi(e);  // tuning
+  if (const char* e = getenv("PP_SCAN_STEPS_N")) d.scan_steps_n = atoi(e);
   return d;
 }
 
@@ -1653,6 +1657,9 @@ extern "C" int pp_debug_cta_records(long long* scan, long long* value, long long
 #endif
 
 #ifdef PP_PHASE_CLOCKS
+extern "C" int pp_debug_warp_records(long long* out) {
+  return cudaMemcpyFromSymbol(out, pp::g_warp_rec, sizeof(pp::g_warp_rec)) == cudaSuccess ? 0 : -1;
+}
 extern "C" int pp_debug_lane_records(int* out) {
   return cudaMemcpyFromSymbol(out, pp::g_lane_rec, sizeof(pp::g_lane_rec)) == cudaSuccess ? PP_OK
                                                                                           : PP_CUDA;

@@ -96,6 +96,16 @@ for i in top:
     t, r = divmod(i, nr)
     print(f" slow: tile {t} robot {r} cyc {cy[i]:.0f} maxsteps {ms[i]:.0f} rounds {rd[i]:.0f} "
           f"lbrej max {L[t, r, :, 2].max()} skip max {L[t, r, :, 1].max()}")
+lib.pp_debug_warp_records.argtypes = [C.POINTER(C.c_longlong)]
+W = np.zeros((1024, 16, 4), np.int64)
+lib.pp_debug_warp_records(W.ctypes.data_as(C.POINTER(C.c_longlong)))
+W = W[:256, :nr]
+print("warp plain steps", pct(W[..., 0].ravel()), " coop steps", pct(W[..., 1].ravel()))
+print("cyc/plain step (no coop warps)", pct((W[..., 3] / np.maximum(W[..., 0], 1))[W[..., 1] == 0]))
+for i in top:
+    t, r = divmod(i, nr)
+    print(f" slow: tile {t} robot {r} plain {W[t, r, 0]} coop {W[t, r, 1]} first coop at cyc "
+          f"{W[t, r, 2]} total {W[t, r, 3]}")
 # by robot
 print("per robot mean cycles:", np.round(R.mean(0)).astype(int).tolist())
 print("per robot mean maxsteps:", np.round(it.max(-1).mean(0), 1).tolist())
