@@ -380,6 +380,8 @@ pp::DevParams make_dev_params(const pp_params& p, const pp_search_grid& g) {
   d.scan_steps_n = 1 << 30;
   if (const char* e = getenv("PP_SCAN_STEPS_W")) d.scan_steps_w = atoi(e);  // tuning
   if (const char* e = getenv("PP_SCAN_STEPS_N")) d.scan_steps_n = atoi(e);
+  d.scan_round_steps = 4;
+  if (const char* e = getenv("PP_SCAN_ROUND")) d.scan_round_steps = atoi(e);
   return d;
 }
 
@@ -1657,6 +1659,9 @@ extern "C" int pp_debug_cta_records(long long* scan, long long* value, long long
 #endif
 
 #ifdef PP_PHASE_CLOCKS
+extern "C" int pp_debug_champ_records(long long* out) {
+  return cudaMemcpyFromSymbol(out, pp::g_champ_rec, sizeof(pp::g_champ_rec)) == cudaSuccess ? 0 : -1;
+}
 extern "C" int pp_debug_warp_records(long long* out) {
   return cudaMemcpyFromSymbol(out, pp::g_warp_rec, sizeof(pp::g_warp_rec)) == cudaSuccess ? 0 : -1;
 }

@@ -46,8 +46,19 @@ def report(label, n_scan, n_value, n_robots):
     print(f" scan: {n_scan} CTAs span {(s[:, 7].max() - t0) / 1e3:.1f} us; "
           f"CTA us {pct((s[:, 7] - s[:, 0]) / 1e3)}")
     print(f"   start offsets us: {pct((s[:, 0] - t0) / 1e3)}; SMs used {len(set(s[:, 6]))}")
-    print(f"   A cyc {pct(s[:, 1])}\n   B cyc {pct(s[:, 2])}\n   C champions {pct(s[:, 4])}\n"
-          f"   C stores+atomics {pct(s[:, 5])}\n   C queue {pct(s[:, 3])}")
+    print(f"   lane-per-cell cyc {pct(s[:, 1])}\n   leftovers cyc {pct(s[:, 2])}\n"
+          f"   champions cyc {pct(s[:, 3])}\n   leftover pairs {pct(s[:, 4])}\n"
+          f"   window (A, part of phase 1) cyc {pct(s[:, 5])}")
+    lib.pp_debug_champ_records.argtypes = [C.POINTER(C.c_longlong)]
+    CR = np.zeros((8192, 4), np.int64)
+    lib.pp_debug_champ_records(CR.ctypes.data_as(C.POINTER(C.c_longlong)))
+    CR = CR[:n_scan]
+    print(f"   champ outside marks {pct(s[:, 3] - (CR[:, 3] - CR[:, 0]))}\n   entry+argmin {pct(CR[:, 1] - CR[:, 0])} rx+stores "
+          f"{pct(CR[:, 2] - CR[:, 1])} atomics+queue {pct(CR[:, 3] - CR[:, 2])}")
+    sl = np.argsort(s[:, 7] - s[:, 0])[-5:]
+    for i in sl:
+        print(f"   slow CTA {i}: us {(s[i, 7] - s[i, 0]) / 1e3:.1f} phase1 {s[i, 1]} left {s[i, 2]} "
+              f"champ {s[i, 3]} n_left {s[i, 4]}")
     rm = r.max(1)
     print(f"   robot-warp cyc {pct(r.ravel())}; per-CTA max/mean {np.mean(rm / r.mean(1)):.2f}")
     if len(v):
