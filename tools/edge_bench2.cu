@@ -8,6 +8,7 @@
 
 using namespace pp;
 
+__device__ long long g_st[4];
 template <int kMode, int kLanes>
 __global__ void k(const FrameDev* F_, double r_lt2, double mb_le2, long long* cyc, double* out) {
   __shared__ FrameDev F;
@@ -39,9 +40,12 @@ __global__ void k(const FrameDev* F_, double r_lt2, double mb_le2, long long* cy
                                  pi.margin)
                  : xd(0.0);
     } else {
+      long long st[4] = {0, 0, 0, 0};
       y = active ? interval_edge_split(V, cx, cy, edge, pi.first, pi.last, pi.fast, pi.y1, pi.y2,
-                                       pi.margin)
+                                       pi.margin, kLanes == 1 ? st : nullptr)
                  : xd(0.0);
+      if (kLanes == 1 && active)
+        for (int q = 0; q < 4; ++q) atomicAdd((unsigned long long*)&g_st[q], (unsigned long long)st[q]);
     }
     acc += y.v;
   }
@@ -79,6 +83,9 @@ int main() {
     for (int i = 0; i < nb * 32; ++i) act += ho[mode][i] != -999.0;
     printf("mode %d: active lanes %d/%d, warp cycles mean %.0f max %lld\n", mode, act, nb * 32, s / nb, mx);
   }
+  long long hst[4];
+  cudaMemcpyFromSymbol(hst, g_st, sizeof(hst));
+  printf("1-lane totals (2 reps x 64 edges pairs): first-run cyc %lld cheap steps %lld exact rounds %lld exact-phase cyc %lld\n", hst[0], hst[1], hst[2], hst[3]);
   int diff = 0;
   for (int i = 0; i < nb * 32; ++i) diff += ho[0][i] != ho[1][i];
   printf("mismatches %d; %s\n", diff, cudaGetErrorString(cudaGetLastError()));
