@@ -782,9 +782,9 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   ctx->last_valid = true;
   const bool all = (copy_flags & PP_COPY_ALL) != 0;
   char* hblk = static_cast<char*>(block);
-  // A pinned block (pp_host_alloc) is device-addressable: the scan kernel
-  // then writes the per-cell outputs straight into it over PCIe while it
-  // runs, and only the score array and the summary are copied afterwards.
+  // A pinned block (pp_host_alloc) is device-addressable: the kernels then
+  // write the per-cell outputs, the scores and the summary straight into it
+  // over PCIe while they run, and the call has no device-to-host copy.
   bool pinned = false;
   {
     cudaPointerAttributes pa{};
@@ -794,7 +794,10 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   }
   const bool direct = all && pinned;
   pp::CellOut co_run = co;
+  // a pinned block also takes the summary straight from the fold
+  pp_dpps_summary* sum_run = pinned ? reinterpret_cast<pp_dpps_summary*>(block) : dsum;
   if (direct) {
+    co_run.score = reinterpret_cast<float*>(hblk + off.score);
     co_run.our_time = reinterpret_cast<double*>(hblk + off.our_time);
     co_run.opp_time = reinterpret_cast<double*>(hblk + off.opp_time);
     co_run.rx = reinterpret_cast<double*>(hblk + off.rx);
@@ -809,13 +812,10 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
     cudaError_t e = cudaMemcpyAsync(ctx->frame.p, F, sizeof(pp::FrameDev), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess)
       e = launch_pipeline<true>(ctx, static_cast<const pp::FrameDev*>(ctx->frame.p), 1, P,
-                                ctx->last_threads, co_run, dsum);
-    if (e == cudaSuccess)
+                                ctx->last_threads, co_run, sum_run);
+    if (e == cudaSuccess && !pinned)
       e = cudaMemcpyAsync(block, dblk, sizeof(pp_dpps_summary), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && direct)
-      e = cudaMemcpyAsync(hblk + off.score, dblk + off.score, off.our_slot - off.score,
-                          cudaMemcpyDeviceToHost, s);
-    else if (e == cudaSuccess && all)
+    if (e == cudaSuccess && all && !direct)
       e = cudaMemcpyAsync(hblk + off.our_time, dblk + off.our_time, off.total - off.our_time,
                           cudaMemcpyDeviceToHost, s);
     return e;
