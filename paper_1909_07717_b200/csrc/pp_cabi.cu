@@ -1662,6 +1662,9 @@ extern "C" int pp_debug_cta_records(long long* scan, long long* value, long long
 extern "C" int pp_debug_champ_records(long long* out) {
   return cudaMemcpyFromSymbol(out, pp::g_champ_rec, sizeof(pp::g_champ_rec)) == cudaSuccess ? 0 : -1;
 }
+extern "C" int pp_debug_d1_records(long long* out) {
+  return cudaMemcpyFromSymbol(out, pp::g_d1_rec, sizeof(pp::g_d1_rec)) == cudaSuccess ? 0 : -1;
+}
 extern "C" int pp_debug_warp_records(long long* out) {
   return cudaMemcpyFromSymbol(out, pp::g_warp_rec, sizeof(pp::g_warp_rec)) == cudaSuccess ? 0 : -1;
 }

@@ -55,6 +55,36 @@ __global__ void k(const FrameDev* F_, double r_lt2, double mb_le2, long long* cy
   if (lane == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+
+template <int kLanes>
+__global__ void kp(const FrameDev* F_, double r_lt2, double mb_le2, long long* cyc, double* out) {
+  __shared__ FrameDev F;
+  __shared__ double hts[kMaxHeights];
+  load_frame(&F, F_);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const ViewCtx V0 = make_view_ctx(0.0, 0.0, F, 0.09, r_lt2, mb_le2);
+  for (int i = threadIdx.x; i < V0.nh; i += blockDim.x) hts[i] = view_height(i, V0.n_half, V0.gh).v;
+  __syncthreads();
+  const double t = lane + 32.0 * blockIdx.x;
+  auto h = [&](double k) { const double x = sin(t * 12.9898 + k * 78.233) * 43758.5453; return x - floor(x); };
+  const xd px = -2.0 + 5.0 * h(1), py = -2.0 + 4.0 * h(2);
+  const double gy = -0.8 + 1.6 * h(3), f = 0.3 + 0.5 * h(4), off = (h(5) - 0.5) * 0.1;
+  const xd cx = px.v + f * (6.0 - px.v), cy = py.v + f * (gy - py.v) + off;
+  const ViewCtx V = make_view_ctx(px, py, F, 0.09, r_lt2, mb_le2, hts);
+  __syncwarp();
+  const long long t0 = clock64();
+  int st = -1;
+  if (lane < kLanes) {
+    const PairInfo pi = pair_info(V, cx, cy);
+    st = pi.status + 4 * pi.first;
+  }
+  __syncwarp();
+  const long long t1 = clock64();
+  out[blockIdx.x * 32 + lane] = st;
+  if (lane == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 int main() {
   FrameDev F{};
   F.L = 12.0; F.W = 9.0; F.gw = 1.8;
@@ -86,6 +116,17 @@ int main() {
   long long hst[4];
   cudaMemcpyFromSymbol(hst, g_st, sizeof(hst));
   printf("1-lane totals (2 reps x 64 edges pairs): first-run cyc %lld cheap steps %lld exact rounds %lld exact-phase cyc %lld\n", hst[0], hst[1], hst[2], hst[3]);
+  for (int m = 0; m < 2; ++m) {
+    for (int rep = 0; rep < 2; ++rep) {
+      if (m == 0) kp<1><<<nb, 32>>>(dF, r_lt2, mb_le2, cyc, out);
+      else kp<32><<<nb, 32>>>(dF, r_lt2, mb_le2, cyc, out);
+    }
+    cudaDeviceSynchronize();
+    cudaMemcpy(hc, cyc, sizeof(hc), cudaMemcpyDeviceToHost);
+    double s = 0;
+    for (int i = 0; i < nb; ++i) s += hc[i];
+    printf("pair_info %d lanes: warp cycles mean %.0f\n", m ? 32 : 1, s / nb);
+  }
   int diff = 0;
   for (int i = 0; i < nb * 32; ++i) diff += ho[0][i] != ho[1][i];
   printf("mismatches %d; %s\n", diff, cudaGetErrorString(cudaGetLastError()));
