@@ -65,7 +65,7 @@ def report(label, n_scan, n_value, n_robots):
         print(f" value: {len(v)} CTAs start {(v[:, 0].min() - t0) / 1e3:.1f} us, end "
               f"{(v[:, 7].max() - t0) / 1e3:.1f} us (gap after scan "
               f"{(v[:, 0].min() - s[:, 7].max()) / 1e3:.1f} us); CTA us {pct((v[:, 7] - v[:, 0]) / 1e3)}")
-        print(f"   D1 {pct(v[:, 1])}\n   D2 {pct(v[:, 2])}\n   D3 {pct(v[:, 3])}\n   red {pct(v[:, 4])}")
+        print(f"   D1 {pct(v[:, 1])}\n   D2 {pct(v[:, 2])}\n   D3a {pct(v[:, 5])}\n   D3b {pct(v[:, 3])}\n   red {pct(v[:, 4])}")
         late = np.argsort(v[:, 7])[-5:]
         for i in late:
             print(f"   late CTA: start {(v[i, 0] - t0) / 1e3:.1f} end {(v[i, 7] - t0) / 1e3:.1f} us "
