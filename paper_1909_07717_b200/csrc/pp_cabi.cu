@@ -538,11 +538,21 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   auto* fc = static_cast<pp::FrameCounters*>(ctx->fcount.p);
   const int64_t chunks = chunks_for(P);
   auto* parts = static_cast<pp::Partial*>(ctx->partials.p);
-  if (ctas >= 2 * 148 * pp::kScanCtasNarrow) {
+  static const int force_shape = [] {  // dev: PP_SCAN_SHAPE=w|m|n
+    const char* e = getenv("PP_SCAN_SHAPE");
+    return e ? (e[0] == 'n' ? 2 : e[0] == 'w' ? 1 : e[0] == 'm' ? 3 : 0) : 0;
+  }();
+  if (force_shape == 2 || (force_shape == 0 && ctas >= 2 * 148 * pp::kScanCtasNarrow)) {
     // Throughput (>= 2 waves of the narrow shape): 4-warp CTAs, 8 per SM,
     // robots round-robin over the warps.
     const int w = n_scan < pp::kScanWarpsNarrow ? n_scan : pp::kScanWarpsNarrow;
     pp::scan_kernel<kCells, pp::kScanWarpsNarrow, pp::kScanCtasNarrow>
+        <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, P, co, q, fc);
+  } else if (force_shape == 3 || (force_shape == 0 && ctas > 148 * pp::kScanCtasWide)) {
+    // More tiles than one wave of the wide shape: 8-warp CTAs, 4 per SM
+    // (one wave up to 592 tiles), robots two per warp, same leftover rounds.
+    const int w = n_scan < pp::kScanWarpsMid ? n_scan : pp::kScanWarpsMid;
+    pp::scan_kernel<kCells, pp::kScanWarpsMid, pp::kScanCtasMid, true>
         <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, P, co, q, fc);
   } else {
     // Latency: 16-warp CTAs, one robot per warp.

@@ -9,10 +9,10 @@ w, p, grid, k, _ = case_inputs(g, "f8")
 for chip in (0, 1):
     grid.chip = chip
     for _ in range(3): st, blk = run_product(lib, ctx, w, p, grid, k)
-    ts=[]; 
-    for _ in range(20):
-        t=time.perf_counter(); st, blk = run_product(lib, ctx, w, p, grid, k); ts.append(time.perf_counter()-t)
-    print("chip", chip, "st", st, "dev ms", blk.summary.device_ms, "wall ms med", 1e3*np.median(ts), "feas", list(blk.summary.n_feasible))
+    ts=[]; ds=[]
+    for _ in range(40):
+        t=time.perf_counter(); st, blk = run_product(lib, ctx, w, p, grid, k); ts.append(time.perf_counter()-t); ds.append(blk.summary.device_ms)
+    print("chip", chip, "st", st, "dev ms med", round(float(np.median(ds)), 5), "wall ms med", 1e3*np.median(ts), "feas", list(blk.summary.n_feasible))
 # C3
 grid.chip = 0; grid.n_directions = 1200; grid.n_powers = 900
 for _ in range(2): st, blk = run_product(lib, ctx, w, p, grid, k)
