@@ -99,6 +99,9 @@ struct pp_ctx {
 
 namespace {
 
+// single-frame staging: FrameDev, then the frame's RobotK[kMaxRobots]
+constexpr size_t kFrameBytes = sizeof(pp::FrameDev) + sizeof(pp::RobotK) * pp::kMaxRobots;
+
 pp_status fail(pp_ctx* ctx, pp_status st, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -718,8 +721,8 @@ pp_status pp_ctx_create(int device, pp_ctx** out) {
   if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
       cudaEventCreate(&ctx->evm) != cudaSuccess)
     return PP_CUDA;
-  if (ctx->frame.reserve(sizeof(pp::FrameDev)) != cudaSuccess) return PP_CUDA;
-  if (ctx->frame_h.reserve(sizeof(pp::FrameDev)) != cudaSuccess) return PP_CUDA;
+  if (ctx->frame.reserve(kFrameBytes) != cudaSuccess) return PP_CUDA;
+  if (ctx->frame_h.reserve(kFrameBytes) != cudaSuccess) return PP_CUDA;
   *out = ctx.release();
   return PP_OK;
 }
@@ -768,6 +771,11 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   }
   pp::DevParams P = make_dev_params(*params, g);
   PP_CUDA_TRY(ctx, ensure_tables(ctx, &P));
+  {  // the frame's robot filter constants travel with it (no per-tile recompute)
+    auto* rk = reinterpret_cast<pp::RobotK*>(reinterpret_cast<char*>(F) + sizeof(pp::FrameDev));
+    for (int ri = 0; ri < F->n_scan; ++ri) pp::robot_consts(*F, P, ri, &rk[ri]);
+    P.rk_pre = static_cast<char*>(ctx->frame.p) + sizeof(pp::FrameDev);
+  }
   PP_CUDA_TRY(ctx, ctx->block.reserve(off.total));
   PP_CUDA_TRY(ctx, reserve_pipeline(ctx, P, 1));
   HT(2);
@@ -819,7 +827,7 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   HT(3);
   // (summary.device_ms is the kernels' own span, measured on the device)
   auto enqueue = [&]() -> cudaError_t {
-    cudaError_t e = cudaMemcpyAsync(ctx->frame.p, F, sizeof(pp::FrameDev), cudaMemcpyHostToDevice, s);
+    cudaError_t e = cudaMemcpyAsync(ctx->frame.p, F, kFrameBytes, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess)
       e = launch_pipeline<true>(ctx, static_cast<const pp::FrameDev*>(ctx->frame.p), 1, P,
                                 ctx->last_threads, co_run, sum_run);
@@ -1674,6 +1682,9 @@ extern "C" int pp_debug_champ_records(long long* out) {
 }
 extern "C" int pp_debug_d1_records(long long* out) {
   return cudaMemcpyFromSymbol(out, pp::g_d1_rec, sizeof(pp::g_d1_rec)) == cudaSuccess ? 0 : -1;
+}
+extern "C" int pp_debug_win_records(long long* out) {
+  return cudaMemcpyFromSymbol(out, pp::g_win_rec, sizeof(pp::g_win_rec)) == cudaSuccess ? 0 : -1;
 }
 extern "C" int pp_debug_warp_records(long long* out) {
   return cudaMemcpyFromSymbol(out, pp::g_warp_rec, sizeof(pp::g_warp_rec)) == cudaSuccess ? 0 : -1;

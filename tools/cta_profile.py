@@ -55,6 +55,12 @@ def report(label, n_scan, n_value, n_robots):
     CR = CR[:n_scan]
     print(f"   champ outside marks {pct(s[:, 3] - (CR[:, 3] - CR[:, 0]))}\n   entry+argmin {pct(CR[:, 1] - CR[:, 0])} rx+stores "
           f"{pct(CR[:, 2] - CR[:, 1])} atomics+queue {pct(CR[:, 3] - CR[:, 2])}")
+    lib.pp_debug_win_records.argtypes = [C.POINTER(C.c_longlong)]
+    WR = np.zeros((8192, 4), np.int64)
+    lib.pp_debug_win_records(WR.ctypes.data_as(C.POINTER(C.c_longlong)))
+    WR = WR[:n_scan]
+    print(f"   frame load {pct(WR[:, 2] - WR[:, 3])}\n   window (warp 0) {pct(WR[:, 0] - WR[:, 2])}\n"
+          f"   robot consts (warp 1) {pct(WR[:, 1] - WR[:, 2])}")
     sl = np.argsort(s[:, 7] - s[:, 0])[-5:]
     for i in sl:
         print(f"   slow CTA {i}: us {(s[i, 7] - s[i, 0]) / 1e3:.1f} phase1 {s[i, 1]} left {s[i, 2]} "
