@@ -61,7 +61,15 @@ def report(label, n_scan, n_value, n_robots):
     WR = WR[:n_scan]
     print(f"   frame load {pct(WR[:, 2] - WR[:, 3])}\n   window (warp 0) {pct(WR[:, 0] - WR[:, 2])}\n"
           f"   robot consts (warp 1) {pct(WR[:, 1] - WR[:, 2])}")
+    lib.pp_debug_round_records.argtypes = [C.POINTER(C.c_longlong)]
+    RR = np.zeros((8192, 8, 2), np.int64)
+    lib.pp_debug_round_records(RR.ctypes.data_as(C.POINTER(C.c_longlong)))
+    RR = RR[:n_scan]
     sl = np.argsort(s[:, 7] - s[:, 0])[-5:]
+    for i in sl:
+        nr = int(s[i, 4] // 10000) + 1
+        parts = [f"{RR[i, r, 0]}@{RR[i, r + 1, 1] - RR[i, r, 1] if r + 1 < nr else 0}" for r in range(min(nr, 8))]
+        print(f"   slow CTA {i} rounds (open pairs@cycles): {' '.join(parts)}")
     for i in sl:
         print(f"   slow CTA {i}: us {(s[i, 7] - s[i, 0]) / 1e3:.1f} phase1 {s[i, 1]} left {s[i, 2]} "
               f"champ {s[i, 3]} n_left {s[i, 4]}")
