@@ -1686,6 +1686,9 @@ extern "C" int pp_debug_d1_records(long long* out) {
 extern "C" int pp_debug_win_records(long long* out) {
   return cudaMemcpyFromSymbol(out, pp::g_win_rec, sizeof(pp::g_win_rec)) == cudaSuccess ? 0 : -1;
 }
+extern "C" int pp_debug_round_records(long long* out) {
+  return cudaMemcpyFromSymbol(out, pp::g_round_rec, sizeof(pp::g_round_rec)) == cudaSuccess ? 0 : -1;
+}
 extern "C" int pp_debug_warp_records(long long* out) {
   return cudaMemcpyFromSymbol(out, pp::g_warp_rec, sizeof(pp::g_warp_rec)) == cudaSuccess ? 0 : -1;
 }
