@@ -379,12 +379,18 @@ pp::DevParams make_dev_params(const pp_params& p, const pp_search_grid& g) {
   d.kt_chip1 = 1;
   d.n_ptiles = (g.n_powers + 31) / 32;
   d.n_tiles = d.n_kt * g.n_directions * d.n_ptiles;
-  d.scan_steps_w = 6;
-  d.scan_steps_n = 1 << 30;
-  if (const char* e = getenv("PP_SCAN_STEPS_W")) d.scan_steps_w = atoi(e);  // tuning
-  if (const char* e = getenv("PP_SCAN_STEPS_N")) d.scan_steps_n = atoi(e);
-  d.scan_round_steps = 4;
-  if (const char* e = getenv("PP_SCAN_ROUND")) d.scan_round_steps = atoi(e);
+  // Leftover-round schedule (tuned on C1/C2; PP_SCAN_STEPS / PP_SCAN_ROUND
+  // override it for experiments, read once)
+  static const int steps = [] {
+    const char* e = getenv("PP_SCAN_STEPS");
+    return e ? atoi(e) : 6;
+  }();
+  static const int round_steps = [] {
+    const char* e = getenv("PP_SCAN_ROUND");
+    return e ? atoi(e) : 4;
+  }();
+  d.scan_steps = steps;
+  d.scan_round_steps = round_steps;
   return d;
 }
 
