@@ -410,13 +410,19 @@ def run_extras(lib, ctx, w, p, kicker):
         pp.thresholds.grid_step = step
         nv = C.c_int64()
         lib.pp_runmap_count(C.byref(w), C.byref(pp), 0xF, C.byref(nv))
-        rblk = abi.RunmapBlock(nv.value)
+        # the caller's result block in pinned memory (as for the DPPS e2e):
+        # the kernel writes the map straight into it
+        rbytes = abi.runmap_offsets(nv.value)["total"]
+        rptr = lib.pp_host_alloc(rbytes)
         req = abi.RunmapRequest(0xF, 0, 4, 0, 0.0, 0.0, 1)
         ts = []
         for _ in range(5):
             t0 = time.perf_counter()
-            lib.pp_runmap(ctx, C.byref(w), C.byref(pp), C.byref(req), rblk.ptr(), nv.value)
+            st = lib.pp_runmap(ctx, C.byref(w), C.byref(pp), C.byref(req), rptr, nv.value)
             ts.append((time.perf_counter() - t0) * 1e3)
+            if st != 0:
+                raise RuntimeError(lib.pp_last_error(ctx).decode())
+        lib.pp_host_free(rptr)
         ex[f"runmap_{step}m_e2e_ms"] = statistics.median(ts[1:])
         ex[f"runmap_{step}m_vertices"] = nv.value
     return ex

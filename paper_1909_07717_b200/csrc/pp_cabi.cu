@@ -1183,7 +1183,9 @@ pp_status pp_runmap(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   int max_blocks = 1;
   for (int z = 0; z < 4; ++z) max_blocks = std::max(max_blocks, rs.R.blocks_per_zone[z]);
   PP_CUDA_TRY(ctx, ctx->run_partials.reserve(sizeof(pp::RunPartial) * 4 * max_blocks));
-  PP_CUDA_TRY(ctx, ctx->run_counter.reserve(sizeof(unsigned) * 4));
+  PP_CUDA_TRY(ctx, ctx->run_counter.reserve(sizeof(unsigned) * 4));  // done count, pad, u64 scorable
+  // (the map is written in device memory and copied in one DMA transfer:
+  // tens of MB of per-thread stores straight into host memory are slower)
   char* d = static_cast<char*>(ctx->run_block.p);
   pp::RunOut ro;
   ro.px = reinterpret_cast<double*>(d + off.px);
@@ -1212,16 +1214,13 @@ pp_status pp_runmap(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   pp_runmap_summary& S = *v.summary;
   S.cut_x = rs.cut_x;
   S.cut_y = rs.cut_y;
-  S.n_vertices = n_map;
-  S.n_scorable = 0;
+  S.n_vertices = n_map;  // (n_scorable: counted by the kernel)
   for (int z = 0; z < 4; ++z) {
     const bool in_map = (req->zone_mask >> z) & 1u;
     S.zone_nx[z] = in_map ? rs.R.zone[z].nx : 0;
     S.zone_ny[z] = in_map ? rs.R.zone[z].ny : 0;
     S.zone_offset[z] = rs.R.zone[z].offset;
   }
-  if (want_map)
-    for (int64_t i = 0; i < n_map; ++i) S.n_scorable += v.scorable[i];
   S.n_best = 0;
   for (int z = 0; z < 4; ++z) {
     S.best_order[z] = -1;
