@@ -85,7 +85,7 @@ struct pp_ctx {
   // run map
   DevBuf run_block, run_partials, run_counter;
   // batch
-  DevBuf batch_frames, batch_sums;
+  DevBuf batch_frames, batch_sums, batch_rk;
   std::vector<pp::FrameDev> batch_host;
   std::vector<int32_t> batch_kickers, batch_poss;
   int64_t batch_n = 0;
@@ -1332,12 +1332,20 @@ pp_status pp_batch_run(pp_ctx* ctx, const pp_params* params, const pp_search_gri
   int64_t group = (int64_t(1) << 28) / std::max<int64_t>(n_cells, 1);
   group = std::max<int64_t>(1, std::min<int64_t>(group, std::min<int64_t>(n, 4096)));
   PP_CUDA_TRY(ctx, reserve_pipeline(ctx, P, group));
+  PP_CUDA_TRY(ctx, ctx->batch_rk.reserve(sizeof(pp::RobotK) * pp::kMaxRobots * static_cast<size_t>(n)));
+  const auto* frames = static_cast<const pp::FrameDev*>(ctx->batch_frames.p);
+  auto* rk = static_cast<pp::RobotK*>(ctx->batch_rk.p);
   PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, s));
+  // every frame's robot filter constants once, not once per tile
+  pp::robot_consts_kernel<<<static_cast<unsigned>((n * pp::kMaxRobots + 255) / 256), 256, 0, s>>>(
+      frames, P, rk, n);
+  PP_CUDA_TRY(ctx, cudaGetLastError());
   for (int64_t f0 = 0; f0 < n; f0 += group) {
     const int64_t nf = std::min(group, n - f0);
-    PP_CUDA_TRY(ctx, launch_pipeline<false>(
-                         ctx, static_cast<const pp::FrameDev*>(ctx->batch_frames.p) + f0, nf, P,
-                         threads, co, static_cast<pp_dpps_summary*>(ctx->batch_sums.p) + f0));
+    pp::DevParams Pg = P;
+    Pg.rk_pre = rk + f0 * pp::kMaxRobots;
+    PP_CUDA_TRY(ctx, launch_pipeline<false>(ctx, frames + f0, nf, Pg, threads, co,
+                                            static_cast<pp_dpps_summary*>(ctx->batch_sums.p) + f0));
   }
   PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, s));
   PP_CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
