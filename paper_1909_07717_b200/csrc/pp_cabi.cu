@@ -1667,15 +1667,6 @@ extern "C" int pp_debug_phase_cycles(unsigned long long* out, int reset) {
 // Profiling build only: scan counters (iterations, skips, lower-bound
 // rejects, upper-bound accepts, exact FP64 tests, FP64 rounds, sum of per-warp
 // max iterations, robot-warp scans).
-extern "C" int pp_debug_scan_counts(unsigned long long* out, int reset) {
-  if (cudaMemcpyFromSymbol(out, pp::g_scan_counts, 16 * sizeof(unsigned long long)) != cudaSuccess)
-    return PP_CUDA;
-  if (reset) {
-    unsigned long long z[16] = {0};
-    if (cudaMemcpyToSymbol(pp::g_scan_counts, z, sizeof(z)) != cudaSuccess) return PP_CUDA;
-  }
-  return PP_OK;
-}
 #endif
 
 #ifdef PP_PHASE_CLOCKS
@@ -1713,14 +1704,4 @@ extern "C" int pp_debug_lane_records(int* out) {
 
 
 #ifdef PP_PHASE_CLOCKS
-extern "C" int pp_debug_edges(int* out, unsigned* n, int reset) {
-  if (cudaMemcpyFromSymbol(n, pp::g_edge_n, sizeof(unsigned)) != cudaSuccess ||
-      cudaMemcpyFromSymbol(out, pp::g_edge_rec, sizeof(pp::g_edge_rec)) != cudaSuccess)
-    return PP_CUDA;
-  if (reset) {
-    const unsigned z = 0;
-    if (cudaMemcpyToSymbol(pp::g_edge_n, &z, sizeof(z)) != cudaSuccess) return PP_CUDA;
-  }
-  return PP_OK;
-}
 #endif

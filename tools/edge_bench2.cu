@@ -1,12 +1,93 @@
 // Dev tool: D2 (goal-view edge bisection) latency per warp with 32 active
-// lanes of distinct blocking geometry: interval_edge (one divergent loop) vs
-// interval_edge_split (cheap steps, then exact rounds).  Checks both give
-// identical edges.
+// lanes of distinct blocking geometry: interval_edge (one divergent loop,
+// defined here) vs the product's interval_edge_split (band steps, then exact
+// rounds); checks both give identical edges.  Also times pair_info.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -o tools/edge_bench2 tools/edge_bench2.cu
 #include <cstdio>
 #include "../paper_1909_07717_b200/csrc/pp_kernels.cuh"
 
 using namespace pp;
+
+// The straightforward replay of bisect_edge (one loop, band-decided or exact
+// step by step): the reference the product's interval_edge_split is checked
+// against here (same result, bit for bit).
+// Interval edge `edge` (0 = lo, 1 = hi) of a blocking opponent: the end value
+// or the 60-step bisection of bisect_edge (pass_eval.cpp:40-51, 88-92).
+// Replayed exactly: each step's predicate is the reference's FP64 one,
+// except where the fast-path band decides it; once the midpoint rounds onto
+// an end point the state is a fixed point (the remaining steps are no-ops).
+// Inside the band two steps are resolved per round: the midpoint and both
+// possible next midpoints are evaluated together (independent FP64 chains).
+__device__ __forceinline__ xd interval_edge(const ViewCtx& V, xd cx, xd cy, int edge, int first,
+                                            int last, bool fast, xd y1, xd y2, double margin) {
+  if (edge == 0 && first == 0) return -V.gh;
+  if (edge == 1 && last == V.nh - 1) return V.gh;
+  xd y_blocked = edge == 0 ? height_at(V, first) : height_at(V, last);
+  xd y_free = edge == 0 ? height_at(V, first - 1) : height_at(V, last + 1);
+  const double lo_in = y1.v + margin, hi_in = y2.v - margin;
+  const double lo_out = y1.v - margin, hi_out = y2.v + margin;
+  // 0 = surely free, 1 = surely blocked, 2 = needs the exact predicate
+  auto decide = [&](double y) -> int {
+    if (!fast) return 2;
+    if (y > lo_in && y < hi_in) return 1;
+    if (y < lo_out || y > hi_out) return 0;
+    return 2;
+  };
+  int i = 0;
+#pragma unroll 1
+  while (i < 60) {
+    const xd mid = xd(0.5) * (y_blocked + y_free);
+    if (mid.v == y_blocked.v || mid.v == y_free.v) break;
+    const int d0 = decide(mid.v);
+    if (d0 != 2) {
+      if (d0) {
+        y_blocked = mid;
+      } else {
+        y_free = mid;
+      }
+      ++i;
+      continue;
+    }
+    // speculate one level ahead
+    const xd mid_b = xd(0.5) * (mid + y_free);     // next midpoint if `mid` is blocked
+    const xd mid_f = xd(0.5) * (y_blocked + mid);  // next midpoint if `mid` is free
+    bool k0, k1, k2;
+    xd s0 = segment_dist_sq_f(cx, cy, V.px, V.py, V.gx, mid, &k0);
+    xd sb = segment_dist_sq_f(cx, cy, V.px, V.py, V.gx, mid_b, &k1);
+    xd sf = segment_dist_sq_f(cx, cy, V.px, V.py, V.gx, mid_f, &k2);
+    if (!(k0 && k1 && k2)) {  // outside ddiv_fast's range: exact division
+      s0 = segment_dist_sq(cx, cy, V.px, V.py, V.gx, mid);
+      sb = segment_dist_sq(cx, cy, V.px, V.py, V.gx, mid_b);
+      sf = segment_dist_sq(cx, cy, V.px, V.py, V.gx, mid_f);
+    }
+    const bool b0 = s0.v < V.r_lt2;
+    xd nxt;
+    bool bn;
+    if (b0) {
+      y_blocked = mid;
+      nxt = mid_b;
+      const int dn = decide(mid_b.v);
+      bn = dn == 2 ? sb.v < V.r_lt2 : dn == 1;
+    } else {
+      y_free = mid;
+      nxt = mid_f;
+      const int dn = decide(mid_f.v);
+      bn = dn == 2 ? sf.v < V.r_lt2 : dn == 1;
+    }
+    ++i;
+    if (i >= 60) break;
+    if (nxt.v == y_blocked.v || nxt.v == y_free.v) break;
+    if (bn) {
+      y_blocked = nxt;
+    } else {
+      y_free = nxt;
+    }
+    ++i;
+  }
+  return xd(0.5) * (y_blocked + y_free);
+}
+
+
 
 __device__ long long g_st[4];
 template <int kMode, int kLanes>
