@@ -79,6 +79,7 @@ struct pp_ctx {
   // single frame
   DevBuf frame, block, partials, counters, dirs, pows, scratch_in, scratch_out;
   DevBuf queue, fcount;  // scan -> value pipeline (per-frame cell queues, counters)
+  DevBuf chunk_fill;     // single frame: entries written per value chunk (streaming)
   PinnedBuf frame_h;
   int dirs_n = -1;
   std::vector<double> pows_key;  // inputs the power table was built from
@@ -784,6 +785,10 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   }
   PP_CUDA_TRY(ctx, ctx->block.reserve(off.total));
   PP_CUDA_TRY(ctx, reserve_pipeline(ctx, P, 1));
+  if (chunks_for(P) <= 4 * 148) {  // the value grid's wide (streaming) shape, see launch_pipeline
+    PP_CUDA_TRY(ctx, ctx->chunk_fill.reserve(sizeof(unsigned) * static_cast<size_t>(chunks_for(P))));
+    P.chunk_fill = static_cast<unsigned*>(ctx->chunk_fill.p);
+  }
   HT(2);
 
   char* dblk = static_cast<char*>(ctx->block.p);
