@@ -67,13 +67,39 @@ struct PinnedBuf {
 
 }  // namespace
 
+// The arguments and launch shapes of a single-frame pipeline, recorded when
+// pp_dpps captures its graph: per call only the FrameArg parameter changes,
+// so the call updates the two kernel nodes' parameters instead of copying
+// the frame to the device.
+using ScanFn = void (*)(const pp::FrameDev*, pp::DevParams, pp::CellOut, pp::CellQueue,
+                        pp::FrameCounters*, pp::FrameArg);
+using ValueFn = void (*)(const pp::FrameDev*, pp::DevParams, pp::CellQueue, pp::FrameCounters*,
+                         pp::CellOut, pp::Partial*, pp_dpps_summary*, int, pp::FrameDev);
+struct PipeRec {
+  const pp::FrameDev* frames;
+  pp::DevParams P;
+  pp::CellOut co;
+  pp::CellQueue q;
+  pp::FrameCounters* fc;
+  pp::Partial* parts;
+  pp_dpps_summary* sums;
+  int nch;
+  ScanFn scan_fn;
+  ValueFn value_fn;
+  dim3 sgrid, sblock, vgrid, vblock;
+};
+
 struct pp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evm = nullptr;
-  // pp_dpps as one CUDA graph (H2D frame, scan, value, D2H), rebuilt when
-  // its key (params, output pointers, copy flags, ...) changes.
+  // pp_dpps as one CUDA graph (scan, value; a D2H only for pageable
+  // blocks), rebuilt when its key (params, output pointers, copy flags, ...)
+  // changes; each call only rewrites the two kernel nodes' FrameArg.
+  cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  cudaGraphNode_t scan_node = nullptr, value_node = nullptr;
+  PipeRec rec{};
   std::vector<unsigned char> gkey;
   std::string err;
   // single frame
@@ -96,6 +122,7 @@ struct pp_ctx {
   pp::CellOut last_co{};
   pp_dpps_summary* last_dsum = nullptr;
   int last_threads = 0;
+  std::unique_ptr<pp::FrameArg> last_fa{new pp::FrameArg()};  // the frame, as a parameter
 };
 
 namespace {
@@ -538,10 +565,14 @@ pp::CellQueue make_queue(pp_ctx* ctx, const pp::DevParams& P, int64_t n_frames) 
 }
 
 // scan_kernel -> value_kernel for `n_frames` frames (buffers reserved).
+// fa: the single frame as a kernel parameter (P.frame_in_arg), else unused.
 template <bool kCells>
 cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_frames,
                             const pp::DevParams& P, int scan_threads, const pp::CellOut& co,
-                            pp_dpps_summary* sums, cudaEvent_t mid = nullptr) {
+                            pp_dpps_summary* sums, cudaEvent_t mid = nullptr,
+                            const pp::FrameArg* fa = nullptr, PipeRec* rec = nullptr) {
+  static const pp::FrameArg kNoArg{};
+  const pp::FrameArg& arg = fa ? *fa : kNoArg;
   const int n_scan = scan_threads / 32;
   const int64_t ctas = n_frames * P.n_tiles;
   const pp::CellQueue q = make_queue(ctx, P, n_frames);
@@ -552,32 +583,35 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
     const char* e = getenv("PP_SCAN_SHAPE");
     return e ? (e[0] == 'n' ? 2 : e[0] == 'w' ? 1 : e[0] == 'm' ? 3 : 0) : 0;
   }();
+  ScanFn sfn;
+  int w;
   if (force_shape == 2 || (force_shape == 0 && ctas >= 2 * 148 * pp::kScanCtasNarrow)) {
     // Throughput (>= 2 waves of the narrow shape): 4-warp CTAs, 8 per SM,
     // robots round-robin over the warps.
-    const int w = n_scan < pp::kScanWarpsNarrow ? n_scan : pp::kScanWarpsNarrow;
-    pp::scan_kernel<kCells, pp::kScanWarpsNarrow, pp::kScanCtasNarrow>
-        <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, P, co, q, fc);
+    w = n_scan < pp::kScanWarpsNarrow ? n_scan : pp::kScanWarpsNarrow;
+    sfn = pp::scan_kernel<kCells, pp::kScanWarpsNarrow, pp::kScanCtasNarrow>;
   } else if (force_shape == 3 || (force_shape == 0 && ctas > 148 * pp::kScanCtasWide)) {
     // More tiles than one wave of the wide shape: 8-warp CTAs, 4 per SM
     // (one wave up to 592 tiles), robots two per warp, same leftover rounds.
-    const int w = n_scan < pp::kScanWarpsMid ? n_scan : pp::kScanWarpsMid;
-    pp::scan_kernel<kCells, pp::kScanWarpsMid, pp::kScanCtasMid, true>
-        <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, P, co, q, fc);
+    w = n_scan < pp::kScanWarpsMid ? n_scan : pp::kScanWarpsMid;
+    sfn = pp::scan_kernel<kCells, pp::kScanWarpsMid, pp::kScanCtasMid, true>;
   } else {
     // Latency: 16-warp CTAs, one robot per warp.
-    const int w = n_scan < pp::kScanWarpsWide ? n_scan : pp::kScanWarpsWide;
-    pp::scan_kernel<kCells, pp::kScanWarpsWide, pp::kScanCtasWide>
-        <<<static_cast<unsigned>(ctas), 32 * w, 0, ctx->stream>>>(frames, P, co, q, fc);
+    w = n_scan < pp::kScanWarpsWide ? n_scan : pp::kScanWarpsWide;
+    sfn = pp::scan_kernel<kCells, pp::kScanWarpsWide, pp::kScanCtasWide>;
   }
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t scfg{};
+  scfg.gridDim = dim3(static_cast<unsigned>(ctas));
+  scfg.blockDim = dim3(32 * w);
+  scfg.stream = ctx->stream;
+  cudaError_t e = cudaLaunchKernelEx(&scfg, sfn, frames, P, co, q, fc, arg);
   if (e != cudaSuccess) return e;
   if (mid) cudaEventRecord(mid, ctx->stream);
   // Few chunks (one frame): wider CTAs shorten each chunk's chain of
   // dependent items; many chunks: narrower CTAs pack the SMs better.
   const unsigned vctas = static_cast<unsigned>(n_frames * chunks);
   // Programmatic dependent launch: the value grid is launched while the scan
-  // grid drains and waits on it in-kernel (griddepcontrol.wait).
+  // grid drains and waits on it in-kernel.
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -588,21 +622,22 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   cfg.attrs = attr;
   cfg.numAttrs = mid ? 0 : 1;  // (kernel timing splits the two grids)
   const int nch = static_cast<int>(chunks);
-  if (vctas <= 4u * 148u) {
-    cfg.blockDim = dim3(pp::kValueThreadsWide);
-    return cudaLaunchKernelEx(&cfg, pp::value_kernel<kCells, pp::kValueThreadsWide>, frames, P,
-                              q, fc, co, parts, sums, nch);
-  }
-  cfg.blockDim = dim3(pp::kValueThreads);
-  return cudaLaunchKernelEx(&cfg, pp::value_kernel<kCells, pp::kValueThreads>, frames, P, q, fc,
-                            co, parts, sums, nch);
+  const bool wide = vctas <= 4u * 148u;
+  const ValueFn vfn = wide ? pp::value_kernel<kCells, pp::kValueThreadsWide>
+                           : pp::value_kernel<kCells, pp::kValueThreads>;
+  cfg.blockDim = dim3(wide ? pp::kValueThreadsWide : pp::kValueThreads);
+  if (rec)
+    *rec = PipeRec{frames, P, co, q, fc, parts, sums, nch, sfn, vfn,
+                   scfg.gridDim, scfg.blockDim, cfg.gridDim, cfg.blockDim};
+  return cudaLaunchKernelEx(&cfg, vfn, frames, P, q, fc, co, parts, sums, nch, arg.frame);
 }
 
 
 // The single-frame launch of the last pp_dpps call.
 cudaError_t launch_single(pp_ctx* ctx, cudaEvent_t mid = nullptr) {
   return launch_pipeline<true>(ctx, static_cast<const pp::FrameDev*>(ctx->frame.p), 1,
-                               ctx->last_P, ctx->last_threads, ctx->last_co, ctx->last_dsum, mid);
+                               ctx->last_P, ctx->last_threads, ctx->last_co, ctx->last_dsum, mid,
+                               ctx->last_fa.get());
 }
 
 }  // namespace
@@ -742,6 +777,7 @@ void pp_ctx_destroy(pp_ctx* ctx) {
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->evm) cudaEventDestroy(ctx->evm);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->graph) cudaGraphDestroy(ctx->graph);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -778,11 +814,12 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   }
   pp::DevParams P = make_dev_params(*params, g);
   PP_CUDA_TRY(ctx, ensure_tables(ctx, &P));
-  {  // the frame's robot filter constants travel with it (no per-tile recompute)
-    auto* rk = reinterpret_cast<pp::RobotK*>(reinterpret_cast<char*>(F) + sizeof(pp::FrameDev));
-    for (int ri = 0; ri < F->n_scan; ++ri) pp::robot_consts(*F, P, ri, &rk[ri]);
-    P.rk_pre = static_cast<char*>(ctx->frame.p) + sizeof(pp::FrameDev);
-  }
+  // The frame and its robots' filter constants (computed here once, not per
+  // tile) travel in the kernels' FrameArg parameter: no host-to-device copy.
+  pp::FrameArg* fa = ctx->last_fa.get();
+  std::memcpy(&fa->frame, F, sizeof(pp::FrameDev));
+  for (int ri = 0; ri < F->n_scan; ++ri) pp::robot_consts(*F, P, ri, &fa->rk[ri]);
+  P.frame_in_arg = 1;
   PP_CUDA_TRY(ctx, ctx->block.reserve(off.total));
   PP_CUDA_TRY(ctx, reserve_pipeline(ctx, P, 1));
   if (chunks_for(P) <= 4 * 148) {  // the value grid's wide (streaming) shape, see launch_pipeline
@@ -838,10 +875,9 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   HT(3);
   // (summary.device_ms is the kernels' own span, measured on the device)
   auto enqueue = [&]() -> cudaError_t {
-    cudaError_t e = cudaMemcpyAsync(ctx->frame.p, F, kFrameBytes, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess)
-      e = launch_pipeline<true>(ctx, static_cast<const pp::FrameDev*>(ctx->frame.p), 1, P,
-                                ctx->last_threads, co_run, sum_run);
+    cudaError_t e = launch_pipeline<true>(ctx, static_cast<const pp::FrameDev*>(ctx->frame.p), 1,
+                                          P, ctx->last_threads, co_run, sum_run, nullptr, fa,
+                                          &ctx->rec);
     if (e == cudaSuccess && !pinned)
       e = cudaMemcpyAsync(block, dblk, sizeof(pp_dpps_summary), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && all && !direct)
@@ -853,7 +889,8 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
     PP_CUDA_TRY(ctx, enqueue());
     PP_CUDA_TRY(ctx, cudaStreamSynchronize(s));
   } else {
-  // The whole call is one graph: H2D frame -> scan -> value -> D2H.
+  // The whole call is one graph: scan -> value (D2H only for pageable
+  // blocks, which take the plain path above).
   struct Key {
     pp::DevParams P;
     pp::CellOut co;
@@ -881,17 +918,50 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   if (!ctx->gexec || ctx->gkey.size() != sizeof(key) ||
       std::memcmp(ctx->gkey.data(), kb, sizeof(key)) != 0) {
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    if (ctx->graph) cudaGraphDestroy(ctx->graph);
     ctx->gexec = nullptr;
+    ctx->graph = nullptr;
+    ctx->scan_node = ctx->value_node = nullptr;
     ctx->gkey.clear();
     PP_CUDA_TRY(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     cudaError_t e = enqueue();
-    cudaGraph_t graph = nullptr;
-    const cudaError_t e2 = cudaStreamEndCapture(s, &graph);
+    const cudaError_t e2 = cudaStreamEndCapture(s, &ctx->graph);
     if (e == cudaSuccess) e = e2;
-    if (e == cudaSuccess) e = cudaGraphInstantiate(&ctx->gexec, graph, 0);
-    if (graph) cudaGraphDestroy(graph);
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&ctx->gexec, ctx->graph, 0);
+    if (e == cudaSuccess) {  // the two kernel nodes whose FrameArg each call rewrites
+      size_t n = 0;
+      cudaGraphGetNodes(ctx->graph, nullptr, &n);
+      std::vector<cudaGraphNode_t> nodes(n);
+      e = cudaGraphGetNodes(ctx->graph, nodes.data(), &n);
+      for (size_t i = 0; e == cudaSuccess && i < n; ++i) {
+        cudaGraphNodeType t;
+        cudaGraphNodeGetType(nodes[i], &t);
+        if (t != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp{};
+        e = cudaGraphKernelNodeGetParams(nodes[i], &kp);
+        if (kp.func == reinterpret_cast<void*>(ctx->rec.scan_fn)) ctx->scan_node = nodes[i];
+        if (kp.func == reinterpret_cast<void*>(ctx->rec.value_fn)) ctx->value_node = nodes[i];
+      }
+      if (e == cudaSuccess && (!ctx->scan_node || !ctx->value_node)) e = cudaErrorInvalidValue;
+    }
     PP_CUDA_TRY(ctx, e);
     ctx->gkey.assign(kb, kb + sizeof(key));
+  } else {
+    // same graph: only this frame's FrameArg changes
+    PipeRec& r = ctx->rec;
+    void* sargs[] = {&r.frames, &r.P, &r.co, &r.q, &r.fc, fa};
+    cudaKernelNodeParams kp{};
+    kp.func = reinterpret_cast<void*>(r.scan_fn);
+    kp.gridDim = r.sgrid;
+    kp.blockDim = r.sblock;
+    kp.kernelParams = sargs;
+    PP_CUDA_TRY(ctx, cudaGraphExecKernelNodeSetParams(ctx->gexec, ctx->scan_node, &kp));
+    void* vargs[] = {&r.frames, &r.P, &r.q, &r.fc, &r.co, &r.parts, &r.sums, &r.nch, &fa->frame};
+    kp.func = reinterpret_cast<void*>(r.value_fn);
+    kp.gridDim = r.vgrid;
+    kp.blockDim = r.vblock;
+    kp.kernelParams = vargs;
+    PP_CUDA_TRY(ctx, cudaGraphExecKernelNodeSetParams(ctx->gexec, ctx->value_node, &kp));
   }
   HT(4);
   PP_CUDA_TRY(ctx, cudaGraphLaunch(ctx->gexec, s));
