@@ -343,7 +343,8 @@ def run_ours(args, rank, world_size, local_rank):
                        "parallelism": f"replicas x{world_size}"},
             "e2e": {"value": e2e_value, "unit": "pair-evals/s",
                     "p50_ms": statistics.median(e2e_ms),
-                    "h2d_bytes_per_step": C.sizeof(abi.World),
+                    # the packed frame + robot constants, as kernel parameters
+                    "h2d_bytes_per_step": int(lib.pp_dpps_upload_bytes()),
                     "d2h_bytes_per_step": block_bytes},
             "roofline": {"bound": "fp32-core", "achieved": achieved, "peak": peak_tflops,
                          "unit": "TFLOP/s", "frac": achieved / peak_tflops,

@@ -231,6 +231,9 @@ const char* pp_last_error(const pp_ctx* ctx);
 /* KernelBackend::name equivalent (kernel.hpp:50-53): "sm100a". */
 const char* pp_kernel_name(void);
 int pp_abi_version(void);
+/* Host bytes one pp_dpps call sends to the device: the packed frame and its
+ * robots' filter constants, as kernel parameters (no copy node). */
+size_t pp_dpps_upload_bytes(void);
 
 /* Pinned host memory for result blocks / frame arrays (fast DMA). */
 void* pp_host_alloc(size_t bytes);

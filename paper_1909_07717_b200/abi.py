@@ -276,6 +276,8 @@ def _declare(lib):
     lib.pp_kernel_name.restype = C.c_char_p
     lib.pp_host_alloc.argtypes = [C.c_size_t]
     lib.pp_host_alloc.restype = vp
+    lib.pp_dpps_upload_bytes.argtypes = []
+    lib.pp_dpps_upload_bytes.restype = C.c_size_t
     lib.pp_host_free.argtypes = [vp]
     lib.pp_host_free.restype = None
     lib.pp_dpps.argtypes = [vp, _P(World), _P(Params), _P(SearchGrid), _I, C.c_uint32, vp]
@@ -333,7 +335,8 @@ def load_library(path: str = LIB_PATH):
 EXPORTED_SYMBOLS = (
     "pp_params_default", "pp_params_validate", "pp_grid_bytes", "pp_grid_view_of",
     "pp_runmap_bytes", "pp_runmap_view_of", "pp_runmap_count", "pp_ctx_create",
-    "pp_ctx_destroy", "pp_last_error", "pp_kernel_name", "pp_abi_version", "pp_host_alloc",
+    "pp_ctx_destroy", "pp_last_error", "pp_kernel_name", "pp_abi_version",
+    "pp_dpps_upload_bytes", "pp_host_alloc",
     "pp_host_free", "pp_dpps", "pp_dpps_relaunch", "pp_ctx_stream", "pp_dpps_kernel_times",
     "pp_grid_cells", "pp_score_cells", "pp_goal_views", "pp_runmap",
     "pp_dpps_batch", "pp_batch_upload", "pp_batch_run", "pp_batch_download",

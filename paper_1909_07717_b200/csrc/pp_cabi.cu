@@ -668,6 +668,8 @@ extern "C" {
 
 int pp_abi_version(void) { return PP_ABI_VERSION; }
 
+size_t pp_dpps_upload_bytes(void) { return sizeof(pp::FrameArg) + sizeof(pp::FrameDev); }
+
 void* pp_ctx_stream(pp_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
 pp_status pp_dpps_relaunch(pp_ctx* ctx) {
