@@ -59,8 +59,7 @@ def report(label, n_scan, n_value, n_robots):
     WR = np.zeros((8192, 4), np.int64)
     lib.pp_debug_win_records(WR.ctypes.data_as(C.POINTER(C.c_longlong)))
     WR = WR[:n_scan]
-    print(f"   frame load {pct(WR[:, 2] - WR[:, 3])}\n   window (warp 0) {pct(WR[:, 0] - WR[:, 2])}\n"
-          f"   robot consts (warp 1) {pct(WR[:, 1] - WR[:, 2])}")
+    print(f"   window incl. frame-field loads (warp 0, from CTA start) {pct(WR[:, 0] - WR[:, 3])}")
     lib.pp_debug_round_records.argtypes = [C.POINTER(C.c_longlong)]
     RR = np.zeros((8192, 8, 2), np.int64)
     lib.pp_debug_round_records(RR.ctypes.data_as(C.POINTER(C.c_longlong)))
