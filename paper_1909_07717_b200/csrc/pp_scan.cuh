@@ -1,0 +1,1006 @@
+// pp_scan.cuh -- scan_kernel: the SBIP search per tile (dpps.cpp:106-215), its shared
+// memory, leftover rounds, champions and the value queue; profiling hooks.
+#pragma once
+
+#include "pp_view.cuh"
+
+namespace pp {
+
+// ---------------------------------------------------------------------------
+// The DPPS pipeline: scan_kernel (search, dpps.cpp:106-215) appends every
+// feasible cell to a per-frame queue; value_kernel (score_pass + best_pass,
+// pass_eval.cpp:148-187) drains the queue in chunks.  Splitting the two keeps
+// every CTA's threads busy: a scan CTA is one tile with one warp per robot,
+// a value CTA is a full chunk of goal views broken into independent items.
+
+// Two scan CTA shapes (64 registers each): 16 warps x 2 CTAs/SM minimises a
+// single frame's latency (one robot per warp); 4 warps x 8 CTAs/SM maximises
+// throughput when there are many tiles (batches, 1 cm grids).
+constexpr int kScanWarpsWide = 16, kScanCtasWide = 2;
+constexpr int kScanWarpsNarrow = 4, kScanCtasNarrow = 8;
+constexpr int kScanWarpsMid = 8, kScanCtasMid = 4;  // one wave of up to 4 x 148 tiles
+#ifndef PP_VALUE_CHUNK
+#define PP_VALUE_CHUNK 32
+#endif
+#ifndef PP_VALUE_THREADS
+#define PP_VALUE_THREADS 128
+#endif
+constexpr int kChunk = PP_VALUE_CHUNK;           // queued cells per value CTA
+constexpr int kMaxWarps = 16;                    // largest CTA of any pipeline kernel
+constexpr int kValueThreads = PP_VALUE_THREADS;  // threads per value CTA (pair/edge items) ...
+constexpr int kValueThreadsWide = 256;           // ... and for launches of at most a wave
+constexpr int kIvCap = 8 * kChunk;               // blocking-opponent intervals per chunk
+constexpr int kMaxHeights = 129;                 // view heights cached in shared memory
+constexpr int kMaxTeamIv = 16;                  // at most one interval per opponent
+
+// Per-frame counters, zeroed by the value kernel's last CTA (self-cleaning).
+struct FrameCounters {
+  unsigned q_count;     // feasible cells queued
+  unsigned n_feas[2];   // per kick slot
+  unsigned chunks_done;
+  unsigned tiles_done;  // scan tiles whose queue entries are written (streaming value)
+  unsigned pad;
+  unsigned long long t0_inv;  // ~(earliest scan CTA start, globaltimer ns); 0 = none
+};
+
+__device__ __forceinline__ unsigned long long pp_now_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Feasible cells awaiting score_pass; frame f owns entries [f*cap, f*cap+cap).
+struct CellQueue {
+  double* rx;
+  double* ry;
+  double* ot;
+  double* pt;
+  int32_t* cell;
+  int8_t* slot;
+  int64_t cap;
+};
+
+struct CellLane {
+  Traj tr;
+  double ux, uy;          // unit direction
+  double ax, ay, bx, by;  // first / last sample of the window (prune)
+  double rest_x, rest_y;  // rest point
+  int kb, ke;             // window [kb, ke)
+  bool valid, rif;        // power exists / ball rests in the field
+};
+
+struct __align__(16) RobotK {
+  ReachBound rb;
+  ArrivalLB lb;
+  double vbound;   // max(|v|, vmax), intercept.cpp:97
+  float bxf, byf;  // ball - robot in FP32 (sample offsets q = b + u s)
+  float vbf;       // vbound in FP32
+};
+
+// A single frame as a kernel parameter: the world state and the scanned
+// robots' filter constants (5.4 KB of the 32 KB parameter space).
+struct __align__(16) FrameArg {
+  FrameDev frame;
+  RobotK rk[kMaxRobots];
+};
+
+// FP32 filter constants of scanned robot `ri` (once per tile, lane = robot).
+PP_HD void robot_consts(const FrameDev& F, const DevParams& P, int ri,
+                                             RobotK* out) {
+  const int slot = F.scan_slot[ri];
+  const bool theirs = slot >= kTheirs;
+  const xd rvx = F.vx[slot], rvy = F.vy[slot];
+  const xd a = theirs ? P.a_t : P.a_o;
+  const xd b = theirs ? P.b_t : P.b_o;
+  const xd vmax = theirs ? P.vmax_t : P.vmax_o;
+  const xd speed_r = xsqrt(rvx * rvx + rvy * rvy);
+  out->vbound = (speed_r > vmax ? speed_r : vmax).v;
+  out->vbf = static_cast<float>(out->vbound);
+  out->bxf = static_cast<float>((xd(F.ball_x) - xd(F.px[slot])).v);
+  out->byf = static_cast<float>((xd(F.ball_y) - xd(F.py[slot])).v);
+  out->rb = ReachBound(static_cast<float>(speed_r.v), static_cast<float>(a.v),
+                       static_cast<float>(b.v), static_cast<float>(vmax.v));
+  out->lb = ArrivalLB(static_cast<float>(rvx.v), static_cast<float>(rvy.v),
+                      static_cast<float>(speed_r.v), static_cast<float>(a.v),
+                      static_cast<float>(b.v), static_cast<float>(vmax.v));
+}
+
+struct ScanSmem {
+  // A: per-cell window (lane = cell), raw storage (xd has a constructor)
+  __align__(16) unsigned char cl_raw[32 * sizeof(CellLane)];
+  int32_t ke[32];
+  int32_t cap[2][32];  // earliest hit sample per team and cell (team cap)
+  TrajF trf[32];  // FP32 trajectory per cell
+  float2 tile_uf;  // FP32 unit direction of the tile
+  // per scanned robot: FP32 filter constants and the FP64 speed bound
+  RobotK rk[kMaxRobots];
+  // B: per (robot, cell) results
+  double res_t[kMaxRobots][32];
+  int32_t res_k[kMaxRobots][32];
+  // (robot, cell) pairs left for scan_leftovers
+  uint16_t left[kMaxRobots * 32];  // ri << 5 | cell; the next sample waits in res_k
+  unsigned n_left, next_pair;
+  long long tph[4];  // profiling build: phase end clocks
+  FrameDev frame;
+};
+
+__device__ __forceinline__ bool better(double s_new, int64_t c_new, double s_old, int64_t c_old) {
+  // best_pass keeps the first strict max in cell order (pass_eval.cpp:178-185).
+  if (c_old < 0) return c_new >= 0;
+  if (c_new < 0) return false;
+  return s_new > s_old || (s_new == s_old && c_new < c_old);
+}
+
+__device__ __forceinline__ void reset_partial(Partial& p) {
+  for (int s = 0; s < 2; ++s) {
+    p.score[s] = 0.0;
+    p.cell[s] = -1;
+    for (int q = 0; q < 5; ++q) p.feat[s][q] = 0.0;
+    p.n_feasible[s] = 0;
+  }
+}
+
+// Summary rows: 0 = all kick types, 1 = flat, 2 = chip (best_pass x3,
+// passplan_main.cpp:102-104).
+__device__ void write_summary(pp_dpps_summary* S, const Partial& B, const DevParams& P) {
+  for (int k = 0; k < 3; ++k) {
+    S->best_cell[k] = -1;
+    S->best_score[k] = 0.0;
+    S->n_feasible[k] = 0;
+    S->best_features[k] = pp_pass_features{0, 0, 0, 0, 0};
+  }
+  for (int s = 0; s < P.n_kt; ++s) {
+    const int row = (s == 0 ? P.kt_chip0 : P.kt_chip1) ? 2 : 1;
+    S->n_feasible[row] = B.n_feasible[s];
+    S->n_feasible[0] += B.n_feasible[s];
+    if (B.cell[s] < 0) continue;
+    S->best_cell[row] = B.cell[s];
+    S->best_score[row] = B.score[s];
+    S->best_features[row] = pp_pass_features{B.feat[s][0], B.feat[s][1], B.feat[s][2],
+                                              B.feat[s][3], B.feat[s][4]};
+    if (better(B.score[s], B.cell[s], S->best_score[0], S->best_cell[0])) {
+      S->best_cell[0] = B.cell[s];
+      S->best_score[0] = B.score[s];
+      S->best_features[0] = S->best_features[row];
+    }
+  }
+}
+
+// Optional per-phase cycle accounting (build with -DPP_PHASE_CLOCKS).
+#ifdef PP_PHASE_CLOCKS
+__device__ unsigned long long g_phase_cycles[16];
+constexpr int kRecCtas = 8192;
+__device__ long long g_cta_rec[2][kRecCtas][8];   // [scan|value][cta]: t0, phases, smid, t1
+__device__ long long g_robot_rec[kRecCtas][16];   // scan: cycles per robot-warp
+__device__ __forceinline__ long long pp_gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PP_CLOCK_INIT() \
+  long long ph_[8] = {0, 0, 0, 0, 0, 0, 0, 0}; \
+  const long long gt0_ = pp_gtimer(); \
+  long long ph_last_ = clock64()
+#define PP_MARK(i)                              \
+  if (threadIdx.x == 0) {                       \
+    const long long now_ = clock64();           \
+    ph_[i] += now_ - ph_last_;                  \
+    ph_last_ = now_;                            \
+  }
+#define PP_FLUSH(slot0)                                                            \
+  if (threadIdx.x == 0) {                                                          \
+    for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&g_phase_cycles[i_], (unsigned long long)ph_[i_]); \
+    atomicAdd(&g_phase_cycles[slot0], 1ull);                                       \
+    if (blockIdx.x < kRecCtas) {                                                   \
+      long long* r_ = g_cta_rec[slot0 - 8][blockIdx.x];                            \
+      unsigned smid_;                                                              \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));                           \
+      r_[0] = gt0_;                                                                \
+      for (int i_ = 0; i_ < 5; ++i_) r_[1 + i_] = ph_[(slot0 == 8 ? 0 : 3) + i_];   \
+      r_[6] = smid_;                                                               \
+      r_[7] = pp_gtimer();                                                         \
+    }                                                                              \
+  }
+__device__ long long g_d1_rec[512][256][2];
+#define PP_D1_T0() const long long d1t0_ = clock64()
+#define PP_D1_T1(pr, pi)                                                         \
+  {                                                                              \
+    long long d1t1_;                                                             \
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(d1t1_) : "r"(pi.status), "r"(pi.first) : "memory"); \
+    if (blockIdx.x < 512 && pr < 256) {                                          \
+      g_d1_rec[blockIdx.x][pr][0] = d1t1_ - d1t0_;                               \
+      g_d1_rec[blockIdx.x][pr][1] = pi.status + 4 * pi.fast + 8 * (pi.first >= 0); \
+    }                                                                            \
+  }
+#define PP_TMARK(i) \
+  if (threadIdx.x == 0) sm.tph[i] = clock64()
+__device__ long long g_champ_rec[kRecCtas][4];
+__device__ long long g_round_rec[kRecCtas][8][2];  // leftover rounds: open pairs, clock
+__device__ long long g_win_rec[kRecCtas][4];  // window end, consts end, frame in, start
+#define PP_CMARK_W(i) \
+  if ((threadIdx.x & 31) == 0 && blockIdx.x < kRecCtas) g_win_rec[blockIdx.x][i] = clock64()
+#define PP_CMARK(i) \
+  if (threadIdx.x == 0 && blockIdx.x < kRecCtas) g_champ_rec[blockIdx.x][i] = clock64()
+#define PP_ROBOT_START() const long long rb_clk_ = clock64()
+#define PP_ROBOT_END(ri)                                                           \
+  if ((threadIdx.x & 31) == 0 && blockIdx.x < kRecCtas && ri < 16)                 \
+    g_robot_rec[blockIdx.x][ri] = clock64() - rb_clk_
+// per-lane scan counters of the first kLaneRecCtas CTAs: steps, skips,
+// lower-bound rejects, upper-bound accepts, exact tests, warp rounds
+constexpr int kLaneRecCtas = 1024;
+__device__ int g_lane_rec[kLaneRecCtas][16][32][6];
+__device__ long long g_warp_rec[kLaneRecCtas][16][4];  // plain / coop steps, cycle of 1st coop
+#define PP_CNT_DECL() \
+  int c_it = 0, c_skip = 0, c_lbrej = 0, c_ub = 0, c_exact = 0, c_rounds = 0, c_plain = 0, \
+      c_coop = 0;                                                                     \
+  long long c_clk0 = clock64(), c_clk_coop = 0
+#define PP_WCLK(i)
+#define PP_CNT(v) (++(v))
+#define PP_STEP_PLAIN() (++c_plain)
+#define PP_STEP_COOP() \
+  if (!c_coop++) c_clk_coop = clock64()
+#define PP_CNT_FLUSH()                                                              \
+  if (blockIdx.x < kLaneRecCtas && ri < 16) {                                      \
+    int* l_ = g_lane_rec[blockIdx.x][ri][threadIdx.x & 31];                        \
+    l_[0] = c_it; l_[1] = c_skip; l_[2] = c_lbrej; l_[3] = c_ub; l_[4] = c_exact;  \
+    l_[5] = c_rounds;                                                              \
+    if ((threadIdx.x & 31) == 0) {                                                 \
+      long long* w_ = g_warp_rec[blockIdx.x][ri];                                  \
+      w_[0] = c_plain; w_[1] = c_coop; w_[2] = c_clk_coop ? c_clk_coop - c_clk0 : -1; \
+      w_[3] = clock64() - c_clk0;                                                  \
+    }                                                                              \
+  }
+#else
+#define PP_CLOCK_INIT()
+#define PP_MARK(i)
+#define PP_FLUSH(slot0)
+#define PP_CNT_DECL()
+#define PP_WCLK(i)
+#define PP_TMARK(i)
+#define PP_D1_T0()
+#define PP_D1_T1(pr, pi)
+#define PP_CMARK(i)
+#define PP_CMARK_W(i)
+#define PP_ROBOT_START()
+#define PP_ROBOT_END(ri)
+#define PP_CNT(v)
+#define PP_CNT_FLUSH()
+#define PP_STEP_PLAIN()
+#define PP_STEP_COOP()
+#endif
+
+__device__ __forceinline__ void load_frame(FrameDev* dst_, const FrameDev* src_) {
+  const int n = sizeof(FrameDev) / 16;
+  const int4* src = reinterpret_cast<const int4*>(src_);
+  int4* dst = reinterpret_cast<int4*>(dst_);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+// ---- scan: one tile (kick slot, direction, 32 powers) per CTA -------------
+// The frame is in sm.frame.
+// Per-lane (cell) scan window of one tile: A of the scan (ball_model.cpp:
+// 12-43, intercept.cpp:12-25, 47-69; dpps.cpp:119-138).  Lane = power.
+
+
+// ray_exit_distance / travel_time_to_distance (pp_math.cuh) with xdiv.
+__device__ __forceinline__ xd ray_exit_distance_d(xd L, xd W, xd ox, xd oy, xd ux, xd uy) {
+  const xd hx = xd(0.5) * L;
+  const xd hy = xd(0.5) * W;
+  if (!(ox.v >= -hx.v && ox.v <= hx.v && oy.v >= -hy.v && oy.v <= hy.v)) return CUDART_NAN;
+  xd s_exit = kInfD;
+  if (ux.v != 0.0) {
+    const xd c = xdiv((ux.v > 0.0 ? hx : -hx) - ox, ux);
+    if (c < s_exit) s_exit = c;
+  }
+  if (uy.v != 0.0) {
+    const xd c = xdiv((uy.v > 0.0 ? hy : -hy) - oy, uy);
+    if (c < s_exit) s_exit = c;
+  }
+  return s_exit.v < 0.0 ? xd(0.0) : s_exit;
+}
+
+__device__ __forceinline__ xd travel_time_d(const Traj& tr, xd slide, xd roll, xd d) {
+  if (d.v == 0.0) return 0.0;
+  if (d > tr.d_stop) return CUDART_NAN;
+  if (d <= tr.d_se) {
+    const xd rad = tr.speed * tr.speed - xd(2.0) * slide * d;
+    return xdiv(xd(2.0) * d, tr.speed + xsqrt(rad.v < 0.0 ? xd(0.0) : rad));
+  }
+  const xd rem = d - tr.d_se;
+  const xd rad = tr.v1 * tr.v1 - xd(2.0) * roll * rem;
+  return tr.t_se + xdiv(xd(2.0) * rem, tr.v1 + xsqrt(rad.v < 0.0 ? xd(0.0) : rad));
+}
+
+// dd / pr: the tile's direction row and this lane's power row, loaded by the
+// caller ahead of the frame (they do not depend on it).
+__device__ __forceinline__ CellLane cell_window(const FrameDev& F, const DevParams& P,
+                                                const double4& dd, const PowRow& pr, bool valid) {
+  const xd dt = P.dt, slide = P.slide, roll = P.roll;
+  CellLane c;
+  c.valid = valid;
+  c.tr.speed = pr.speed;
+  c.tr.v1 = pr.v1;
+  c.tr.t_se = pr.t_se;
+  c.tr.d_se = pr.d_se;
+  c.tr.t_stop = pr.t_stop;
+  c.tr.d_stop = pr.d_stop;
+  const Traj& tr = c.tr;
+  const xd ux = dd.z, uy = dd.w;
+  const xd ox = F.ball_x, oy = F.ball_y;
+  const xd d_exit = ray_exit_distance_d(F.L, F.W, ox, oy, dd.x, dd.y);
+  int kb = 0, ke = 0;
+  bool rif = false;
+  if (!isnan(d_exit.v)) {
+    ke = pr.count;
+    kb = pr.kb;
+    if (d_exit < tr.d_stop) {
+      const xd t_exit = travel_time_d(tr, slide, roll, d_exit);
+      const int k_last = !isnan(t_exit.v)
+                             ? static_cast<int>(floor((xdiv(t_exit, dt) + xd(1e-9)).v))
+                             : pr.count - 1;
+      ke = ke < k_last + 1 ? ke : k_last + 1;
+    } else {
+      rif = true;
+    }
+  }
+  c.ux = ux.v;
+  c.uy = uy.v;
+  c.kb = kb;
+  c.ke = ke;
+  c.rif = rif;
+  c.rest_x = (ox + ux * tr.d_stop).v;
+  c.rest_y = (oy + uy * tr.d_stop).v;
+  c.ax = c.ay = c.bx = c.by = 0.0;
+  if (kb < ke) {
+    const xd s_lo = distance_at(tr, slide, roll, xd(double(kb)) * dt);
+    const xd s_hi = distance_at(tr, slide, roll, xd(double(ke - 1)) * dt);
+    c.ax = (ox + ux * s_lo).v;
+    c.ay = (oy + uy * s_lo).v;
+    c.bx = (ox + ux * s_hi).v;
+    c.by = (oy + uy * s_hi).v;
+  }
+  return c;
+}
+
+// FP32 sample filter outcome (scan_robot / scan_leftovers).
+enum SampleCode { kNone = 0, kRej = 1, kEnd = 2, kCap = 3, kHit = 4, kCand = 5 };
+
+// Per (robot, tile) FP32 filter constants: the robot's offset from the ball,
+// speed bound and the tile's direction; rb / lb stay in shared memory (rk).
+struct SampleF {
+  float bxf, byf, vbf;  // ball - robot, vbound
+  float uxf, uyf;       // the tile's direction
+  float dtf, radf;
+  float s0;             // ray coordinate of the robot's closest approach
+};
+
+__device__ __forceinline__ SampleF sample_f(const RobotK& rk, float2 uf, const DevParams& P) {
+  SampleF S;
+  S.bxf = rk.bxf;
+  S.byf = rk.byf;
+  S.vbf = rk.vbf;
+  S.uxf = uf.x;
+  S.uyf = uf.y;
+  S.dtf = P.dtf;
+  S.radf = P.radf;
+  S.s0 = -(S.bxf * S.uxf + S.byf * S.uyf);
+  return S;
+}
+
+// One sample kk of a (robot, cell): kRej with the next sample worth looking
+// at in *next (every sample in [kk, *next) certainly infeasible), else the
+// first non-rejected outcome: kEnd (window over), kCap (past the team cap),
+// kHit (certainly feasible), kCand (needs the exact test).
+__device__ __forceinline__ int test_sample(const RobotK& rk, const SampleF& S, int kk,
+                                           const TrajF& tf_, int ke_s, int cap_c, int* next) {
+  if (kk >= ke_s) return kEnd;
+  if (kk > cap_c) return kCap;
+  const float tf = static_cast<float>(kk) * S.dtf;
+  const float sf = tf_.distance_at(tf);
+  const float qxf = fmaf(S.uxf, sf, S.bxf);
+  const float qyf = fmaf(S.uyf, sf, S.byf);
+  const float d2f = fmaf(qxf, qxf, qyf * qyf);
+  const float thr = S.radf + fmaf(rk.rb.reach(tf), 1.0001f, 1e-4f);
+  const float inv_d = rsqrt_ftz(fmaxf(d2f, 1e-30f));
+  const float df = d2f * inv_d;
+  if (d2f > thr * thr) {
+    // Cannot get there.  Skip ahead: the gap d - thr shrinks by at most
+    // (ball approach speed + vbound) * dt per sample; past the closest
+    // approach (s >= s0) the distance cannot shrink.
+    const float gap = df - thr;
+    const float approach = sf < S.s0 + 1e-3f ? tf_.speed_at(tf) : 0.f;
+    const float rate = (approach + S.vbf) * S.dtf * 1.0001f;
+    const float j = floorf(gap * rcp_ftz(rate) * 0.9999f);
+    *next = kk + 1 + (j > 1.f ? (j < 4096.f ? static_cast<int>(j) - 1 : 4095) : 0);
+    return kRej;
+  }
+  if (rk.lb.lower_bound(qxf, qyf, df, inv_d, S.radf) > fmaf(tf, 1.000001f, 1e-6f)) {
+    *next = kk + 1;
+    return kRej;
+  }
+  // certainly feasible: arrival <= t with margin (and then the reference's
+  // quick reject cannot fire: reach - deff >= vbound t / 2)
+  if (rk.lb.upper_bound(qxf, qyf, df, inv_d, S.radf) < fmaf(tf, 0.999999f, -1e-6f)) return kHit;
+  return kCand;
+}
+
+// FP64 state of scanned robot ri for the exact test and the rest rule.
+struct RobotX {
+  xd px, py, vx, vy, a, b, vmax, vbound;
+  int team;
+};
+
+__device__ __forceinline__ RobotX robot_x(const FrameDev& F, const DevParams& P, const RobotK& rk,
+                                          int ri) {
+  RobotX X;
+  const int slot = F.scan_slot[ri];
+  const bool theirs = slot >= kTheirs;
+  X.team = theirs ? 1 : 0;
+  X.px = F.px[slot];
+  X.py = F.py[slot];
+  X.vx = F.vx[slot];
+  X.vy = F.vy[slot];
+  X.a = theirs ? P.a_t : P.a_o;
+  X.b = theirs ? P.b_t : P.b_o;
+  X.vmax = theirs ? P.vmax_t : P.vmax_o;
+  X.vbound = rk.vbound;
+  return X;
+}
+
+// The reference's test of sample k (kernel.hpp:33-44, intercept.cpp:96-113).
+__device__ __forceinline__ bool exact_hit(const CellLane& c, const FrameDev& F, const DevParams& P,
+                                          const RobotX& X, int k) {
+  const xd dt = P.dt, radius = P.radius;
+  const xd t = xd(double(k)) * dt;
+  const xd sx = distance_at(c.tr, P.slide, P.roll, t);
+  const xd qx = (xd(F.ball_x) + xd(c.ux) * sx) - X.px;
+  const xd qy = (xd(F.ball_y) + xd(c.uy) * sx) - X.py;
+  const xd d2 = qx * qx + qy * qy;
+  const xd reach = radius + X.vbound * t;
+  return !(d2 > reach * reach) &&
+         arrival_given(qx, qy, d2, X.vx, X.vy, X.a, X.b, X.vmax, radius) <= t;
+}
+
+// Result of a finished (robot, cell) scan: hit sample, team-capped, else the
+// rest rule (dpps.cpp:177-190).  time +inf = never; code -2 never, -1 rest,
+// -3 capped out, >= 0 hit sample.
+__device__ __forceinline__ void pair_result(const CellLane& c, const DevParams& P, const RobotX& X,
+                                            int hit, bool capped, double* t_out, int* code_out) {
+  double time = CUDART_INF;
+  int code = -2;
+  if (c.valid) {
+    if (hit >= 0) {
+      time = (xd(double(hit)) * xd(P.dt)).v;
+      code = hit;
+    } else if (capped) {
+      code = -3;  // another robot of the team hit strictly earlier
+    } else if (c.rif) {
+      const xd arr = arrival_to_point(c.rest_x, c.rest_y, X.px, X.py, X.vx, X.vy, X.a, X.b,
+                                      X.vmax, P.radius);
+      const xd ts = c.tr.t_stop;
+      time = (arr > ts ? arr : ts).v;
+      code = -1;
+    }
+  }
+  *t_out = time;
+  *code_out = code;
+}
+
+// B of the scan for robot `ri` (one warp, lane = cell): scan_robot
+// (intercept.cpp:87-115) + first feasible sample (kernel.hpp:33-44) + rest
+// rule (dpps.cpp:177-190).  Two exact-safe accelerations, neither of which
+// can change a result:
+//  * team cap (dpps.cpp:142-153): robots of a team share the earliest hit
+//    index per cell (cap[team * 32 + cell], shared memory); a robot stops
+//    once its next sample is past it (it can no longer win or tie).
+//  * FP32 filters: a sample is tested exactly only if the robot could
+//    possibly get there (ReachBound, ArrivalLB); runs of samples are skipped
+//    only when certified infeasible.
+// Lane-per-cell steps, at most max_steps of them: a lane still searching
+// after that returns its next sample in *left_k (the CTA finishes it in
+// scan_leftovers with many lanes per cell); otherwise *left_k = -1 and the
+// result is in *t_out / *code_out.
+__device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_in, const SampleF& S,
+                                           const FrameDev& F, const DevParams& P,
+                                           const RobotK& rk, int* cap,
+                                           int ri, int max_steps, double* t_out,
+                                           int* code_out, int* left_k) {
+  const int lane = threadIdx.x & 31;
+  const bool valid = c.valid;
+  const int kb = c.kb;
+  const int ke = valid ? c.ke : 0;
+  int k = ke;
+  if (valid && kb < ke) {
+    // scan_robot's prunes (intercept.cpp:89-113) in FP32 with 1e-3 m of
+    // slack: the window is skipped, or the scan starts late, only where
+    // every sample certainly fails the quick reject.
+    const int slot = F.scan_slot[ri];
+    const float rx0 = static_cast<float>(F.px[slot]), ry0 = static_cast<float>(F.py[slot]);
+    const float ax = static_cast<float>(c.ax), ay = static_cast<float>(c.ay);
+    const float abx = static_cast<float>(c.bx) - ax;
+    const float aby = static_cast<float>(c.by) - ay;
+    const float len2 = abx * abx + aby * aby;
+    float tt = len2 > 0.f ? __fdividef((rx0 - ax) * abx + (ry0 - ay) * aby, len2) : 0.f;
+    tt = fminf(fmaxf(tt, 0.f), 1.f);
+    const float ex = ax + abx * tt - rx0, ey = ay + aby * tt - ry0;
+    const float gap = sqrt_a(ex * ex + ey * ey) - 1e-3f - S.radf;
+    if (!(gap > S.vbf * static_cast<float>(ke - 1) * S.dtf * 1.0001f)) {
+      k = kb;
+      if (S.vbf > 0.f && gap > 0.f) {
+        const int kk = static_cast<int>(floorf(gap / (S.vbf * S.dtf * 1.0001f))) - 1;
+        k = kk > kb ? (kk < ke ? kk : ke) : kb;
+      }
+    }
+  }
+  const TrajF trf = trf_in;
+  int hit = -1;
+  bool capped = false;
+  int state = k >= ke ? 2 : 0;  // 0 scanning, 1 candidate pending, 2 finished
+  PP_CNT_DECL();
+  // Warp-synchronous: each step every scanning lane examines one sample (or
+  // certifies a run of them infeasible); lanes the FP32 bounds cannot decide
+  // wait as candidates and get the exact FP64 test together when no lane is
+  // scanning.  Team caps are re-read from shared memory every step.
+  const int team = F.scan_slot[ri] >= kTheirs ? 1 : 0;
+  volatile int* vcap = cap + team * 32 + lane;
+  for (int n_step = 0; n_step < max_steps; ++n_step) {
+    const unsigned act = __ballot_sync(0xffffffffu, state == 0);
+    if (act == 0u) {
+      const bool pend = state == 1;
+      if (!__any_sync(0xffffffffu, pend)) break;
+      PP_CNT(c_rounds);
+      if (pend) {
+        PP_CNT(c_exact);
+        if (exact_hit(c, F, P, robot_x(F, P, rk, ri), k)) {
+          hit = k;
+          atomicMin(&cap[team * 32 + lane], k);
+          state = 2;
+        } else {
+          ++k;
+          state = 0;
+        }
+      }
+      continue;
+    }
+    PP_STEP_PLAIN();
+    if (state == 0) {
+      PP_CNT(c_it);
+      int next = k;
+      const int code = test_sample(rk, S, k, trf, ke, *vcap, &next);
+      switch (code) {
+        case kRej:
+          PP_CNT(c_skip);
+          k = next;
+          break;
+        case kEnd: state = 2; break;
+        case kCap: capped = true; state = 2; break;
+        case kHit:
+          PP_CNT(c_ub);
+          hit = k;
+          atomicMin(&cap[team * 32 + lane], k);
+          state = 2;
+          break;
+        default: state = 1; break;  // kCand
+      }
+    }
+  }
+  PP_CNT_FLUSH();
+  if (state != 2) {
+    *left_k = k;
+    return;
+  }
+  *left_k = -1;
+  pair_result(c, P, robot_x(F, P, rk, ri), hit, capped, t_out, code_out);
+}
+
+// Scan pairs left over by scan_robot: left[] holds ri << 5 | cell and
+// res_k[ri][cell] the pair's next sample.
+// Each pair gets a group of g lanes (a power of two, 4..32) testing g
+// consecutive samples per step: the first non-rejected one decides (exact
+// test for a candidate), else the pair advances past every sample the group
+// certified infeasible.  Groups take pairs from the shared list dynamically.
+// All warps of the CTA take part; results go to res_t / res_k.
+__device__ __forceinline__ void scan_leftovers(const CellLane* cl, const TrajF* trf_s,
+                                               const int* ke_s, float2 uf, const FrameDev& F,
+                                               const DevParams& P, const RobotK* rk_s, int* cap,
+                                               const uint16_t* left, int n_left,
+                                               unsigned* next_pair, double (*res_t)[32],
+                                               int32_t (*res_k)[32], int max_steps) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  int g = 32;
+  while (g > 4 && n_left * g > nwarps * 32) g >>= 1;
+  const int gbase = lane & ~(g - 1);
+  const int o = lane - gbase;
+  const unsigned gmask = g == 32 ? 0xffffffffu : ((1u << g) - 1u) << gbase;
+  int pi = -1;      // pair of this group (-1 none / finished the list)
+  int ri = 0, cell = 0, k = 0;
+  int hit = -1, ns = 0;
+  bool capped = false;
+  // every lane calls take(); groups with need == false keep their pair
+  auto take = [&](bool need) {
+    unsigned nx = 0;
+    if (need && o == 0) nx = atomicAdd(next_pair, 1u);
+    nx = __shfl_sync(0xffffffffu, nx, gbase);
+    if (need) {
+      pi = nx < static_cast<unsigned>(n_left) ? static_cast<int>(nx) : -1;
+      if (pi >= 0) {
+        const unsigned w = left[pi];
+        ri = static_cast<int>(w >> 5);
+        cell = static_cast<int>(w & 31u);
+        k = res_k[ri][cell];
+        hit = -1;
+        ns = 0;
+        capped = false;
+      }
+    }
+  };
+  take(true);
+  while (__any_sync(0xffffffffu, pi >= 0)) {
+    int code = kNone, nxt = 0;
+    const RobotK& rk = rk_s[ri];
+    const int team = F.scan_slot[ri] >= kTheirs ? 1 : 0;
+    if (pi >= 0) {
+      const SampleF S = sample_f(rk, uf, P);
+      const int cap_c = *(volatile int*)(cap + team * 32 + cell);
+      code = test_sample(rk, S, k + o, trf_s[cell], ke_s[cell], cap_c, &nxt);
+    }
+    const unsigned nonrej = __ballot_sync(0xffffffffu, code > kRej) & gmask;
+    int reach = code == kRej ? nxt : 0;
+    for (int s = 1; s < g; s <<= 1) reach = max(reach, __shfl_xor_sync(0xffffffffu, reach, s));
+    bool done = false;
+    if (pi >= 0) {
+      if (nonrej) {
+        const int f = __ffs(nonrej) - 1 - gbase;
+        const int gcode = __shfl_sync(gmask, code, gbase + f);
+        const int kk = k + f;
+        if (gcode == kEnd) {
+          done = true;
+        } else if (gcode == kCap) {
+          capped = true;
+          done = true;
+        } else if (gcode == kHit) {
+          hit = kk;
+          done = true;
+        } else {  // kCand: the exact test (same arguments in every lane of the group)
+          const RobotX X = robot_x(F, P, rk, ri);
+          if (exact_hit(cl[cell], F, P, X, kk)) {
+            hit = kk;
+            done = true;
+          } else {
+            k = kk + 1;
+          }
+        }
+      } else {
+        k = max(k + g, reach);
+      }
+    }
+    if (done) {
+      if (o == 0) {
+        if (hit >= 0) atomicMin(&cap[team * 32 + cell], hit);
+        const RobotX X = robot_x(F, P, rk, ri);
+        double t;
+        int cd;
+        pair_result(cl[cell], P, X, hit, capped, &t, &cd);
+        res_t[ri][cell] = t;
+        res_k[ri][cell] = cd;
+      }
+    }
+    // a pair still open after max_steps goes back to the list (next round,
+    // with more lanes per pair once fewer pairs remain)
+    bool release = done;
+    if (pi >= 0 && !done && ++ns >= max_steps) {
+      if (o == 0) res_k[ri][cell] = k;
+      release = true;
+    }
+    if (__any_sync(0xffffffffu, release)) take(release);
+  }
+}
+
+// C of the scan (dpps.cpp:140-213), one warp, lane = cell: our and their
+// champion (strict (time, id) lexicographic argmin seeded with (kNever, -1),
+// so visiting order does not matter), receive point, feasibility; cell
+// outputs, and feasible cells appended to the frame's value queue.
+// res_t(ri) / res_k(ri): this lane's time and code for scanned robot ri.
+template <bool kCells, class ResT, class ResK>
+__device__ __forceinline__ void tile_champions(const CellLane& c, const FrameDev& F,
+                                               const DevParams& P, ResT res_t, ResK res_k,
+                                               const CellOut& out, const CellQueue& q,
+                                               FrameCounters* __restrict__ fc, int f, int kt,
+                                               int64_t cell0) {
+  const int lane = threadIdx.x & 31;
+  const xd dt = P.dt, slide = P.slide, roll = P.roll;
+      // Times are >= 0 or +inf (never NaN, never -0), so their bit patterns
+      // order like the values: the (time, id) argmin runs on integers.
+      const int n_ours_scan = F.n_ours - 1;  // kicker excluded
+      unsigned long long bt_o_bits = 0x7ff0000000000000ull;  // +inf
+      int bid_o = -1, bri_o = -1, bs_o = -1;
+      for (int s = 0; s < F.n_ours; ++s) {
+        if (s == F.kicker_slot) continue;
+        const int ri = s - (s > F.kicker_slot ? 1 : 0);
+        const unsigned long long tb = __double_as_longlong(res_t(ri));
+        const int id = F.id[s];
+        if (tb < bt_o_bits || (tb == bt_o_bits && id < bid_o)) {
+          bt_o_bits = tb;
+          bid_o = id;
+          bri_o = ri;
+          bs_o = s;
+        }
+      }
+      unsigned long long bt_t_bits = 0x7ff0000000000000ull;
+      int bid_t = -1, bs_t = -1;
+      for (int s = 0; s < F.n_theirs; ++s) {
+        const int ri = n_ours_scan + s;
+        const unsigned long long tb = __double_as_longlong(res_t(ri));
+        const int id = F.id[kTheirs + s];
+        if (tb < bt_t_bits || (tb == bt_t_bits && id < bid_t)) {
+          bt_t_bits = tb;
+          bid_t = id;
+          bs_t = s;
+        }
+      }
+      const xd bt_o = __longlong_as_double(static_cast<long long>(bt_o_bits));
+      const xd bt_t = __longlong_as_double(static_cast<long long>(bt_t_bits));
+      const int bk_o = bri_o >= 0 ? res_k(bri_o) : -2;
+      PP_CMARK(1);
+      xd rx = 0.0, ry = 0.0;
+      bool feas = false;
+      if (bt_o.v < CUDART_INF) {
+        if (bk_o >= 0) {
+          const xd s = distance_at(c.tr, slide, roll, xd(double(bk_o)) * dt);
+          rx = xd(F.ball_x) + xd(c.ux) * s;
+          ry = xd(F.ball_y) + xd(c.uy) * s;
+        } else {
+          rx = c.rest_x;
+          ry = c.rest_y;
+        }
+        feas = isinf(bt_t.v) || (bt_o + xd(P.safety) <= bt_t);
+      }
+      feas = feas && c.valid;
+      const int64_t cell = cell0 + lane;
+      PP_CMARK(2);
+      const unsigned fm = __ballot_sync(0xffffffffu, feas);
+      unsigned base = 0;
+      if (lane == 0 && fm) {
+        base = atomicAdd(&fc[f].q_count, static_cast<unsigned>(__popc(fm)));
+        atomicAdd(&fc[f].n_feas[kt], static_cast<unsigned>(__popc(fm)));
+      }
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const unsigned n_new = static_cast<unsigned>(__popc(fm));
+      if (feas) {
+        const int64_t pos = static_cast<int64_t>(f) * q.cap + base + __popc(fm & ((1u << lane) - 1u));
+        q.rx[pos] = rx.v;
+        q.ry[pos] = ry.v;
+        q.ot[pos] = bt_o.v;
+        q.pt[pos] = bt_t.v;
+        q.cell[pos] = static_cast<int32_t>(cell);
+        q.slot[pos] = static_cast<int8_t>(kt);
+      }
+      if (P.chunk_fill) {
+        // publish: entries first (every lane's, ordered by the warp barrier
+        // and lane 0's fence), then the chunks' fill counts, then the tile
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          if (n_new) {
+            const unsigned c0 = base / kChunk, c1 = (base + n_new - 1) / kChunk;
+            const unsigned in0 = min(n_new, (c0 + 1) * kChunk - base);
+            atomicAdd(&P.chunk_fill[c0], in0);
+            if (c1 != c0) atomicAdd(&P.chunk_fill[c1], n_new - in0);
+          }
+          __threadfence();
+          atomicAdd(&fc[f].tiles_done, 1u);
+        }
+      }
+      // The cell outputs last: they may go to host memory (pinned result
+      // block), and the fences above need not wait for those writes.
+      if (kCells && c.valid) {
+        out.our_time[cell] = bt_o.v;
+        out.opp_time[cell] = bt_t.v;
+        out.rx[cell] = rx.v;
+        out.ry[cell] = ry.v;
+        out.our_slot[cell] = static_cast<int8_t>(bs_o);
+        out.opp_slot[cell] = static_cast<int8_t>(bs_t);
+        out.feasible[cell] = feas;
+        if (!feas) out.score[cell] = -CUDART_INF_F;
+      }
+      PP_CMARK(3);
+}
+
+template <bool kCells, bool kLeftovers>
+__device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, const CellOut& out,
+                                          const CellQueue& q, FrameCounters* __restrict__ fc,
+                                          int f, int tile, const double4& dd, const PowRow& pr,
+                                          const FrameDev* src, const RobotK* rk_arg) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const FrameDev& F = sm.frame;
+  const xd dt = P.dt, slide = P.slide, roll = P.roll, radius = P.radius;
+  {
+    const int kt = tile / (P.n_dirs * P.n_ptiles);
+    const int dir = (tile / P.n_ptiles) % P.n_dirs;
+    const int ptile = tile % P.n_ptiles;
+    const int64_t cell0 = (static_cast<int64_t>(kt) * P.n_dirs + dir) * P.n_pows + ptile * 32;
+
+    // ---- A: trajectory + scan window per cell (ball_model.cpp:12-43,
+    //      intercept.cpp:12-25, 47-69; dpps.cpp:119-138) by warp 0, reading
+    //      the ball and field from the frame's source, while the other warps
+    //      stage the frame and the robots' filter constants.
+    if (nwarps == 1) {
+      load_frame(&sm.frame, src);
+      __syncwarp();
+    } else if (warp > 0) {
+      const int4* fs = reinterpret_cast<const int4*>(src);
+      int4* fd = reinterpret_cast<int4*>(&sm.frame);
+      for (int i = threadIdx.x - 32; i < static_cast<int>(sizeof(FrameDev) / 16);
+           i += blockDim.x - 32)
+        fd[i] = fs[i];
+    }
+    if (warp == 0) {
+      const CellLane c = cell_window(*src, P, dd, pr, ptile * 32 + lane < P.n_pows);
+      reinterpret_cast<CellLane*>(sm.cl_raw)[lane] = c;
+      sm.cap[0][lane] = 0x7fffffff;
+      sm.cap[1][lane] = 0x7fffffff;
+      if (lane == 0) {
+        sm.n_left = 0;
+        sm.next_pair = 0;
+      }
+      sm.ke[lane] = c.ke;
+      sm.trf[lane] = TrajF(c.tr, static_cast<float>(slide.v), static_cast<float>(roll.v));
+      if (lane == 0) sm.tile_uf = make_float2(static_cast<float>(c.ux), static_cast<float>(c.uy));
+      PP_CMARK_W(0);
+    }
+    if (rk_arg || P.rk_pre) {
+      // the frame's robot constants (host- or pre-computed): the other warps
+      // stage them while warp 0 computes the windows
+      if (warp > 0 || nwarps == 1) {
+        const int4* rks = rk_arg ? reinterpret_cast<const int4*>(rk_arg)
+                                 : static_cast<const int4*>(P.rk_pre) +
+                                       static_cast<int64_t>(f) * (kMaxRobots * sizeof(RobotK) / 16);
+        int4* dst = reinterpret_cast<int4*>(sm.rk);
+        const int n16 = src->n_scan * static_cast<int>(sizeof(RobotK) / 16);
+        const int t0 = nwarps == 1 ? lane : threadIdx.x - 32;
+        const int nt = nwarps == 1 ? 32 : blockDim.x - 32;
+        for (int i = t0; i < n16; i += nt) dst[i] = rks[i];
+      }
+    } else if (warp == (nwarps > 1 ? 1 : 0)) {
+      for (int ri = lane; ri < src->n_scan; ri += 32) robot_consts(*src, P, ri, &sm.rk[ri]);
+      PP_CMARK_W(1);
+    }
+    __syncthreads();
+    PP_TMARK(2);
+
+  // ---- B: SBIP scan per (robot, cell): scan_robot (intercept.cpp:87-115)
+    //      + first feasible sample (kernel.hpp:33-44) + rest rule
+    //      (dpps.cpp:177-190).
+    //      Two exact-safe accelerations, neither of which can change a result:
+    //      * team cap (dpps.cpp:142-153): robots of a team share the earliest
+    //        hit index per cell in shared memory; a robot stops once its next
+    //        sample is past it (it can no longer win or tie).
+    //      * FP32 reach filter: a sample is only tested exactly if the robot
+    //        could possibly get there, d <= radius + D(t) (ReachBound).
+    const CellLane* cl = reinterpret_cast<const CellLane*>(sm.cl_raw);
+    const int max_steps = kLeftovers ? P.scan_steps : 1 << 30;
+    for (int ri = warp; ri < F.n_scan; ri += nwarps) {
+      const RobotK& rk = sm.rk[ri];
+      const SampleF S = sample_f(rk, sm.tile_uf, P);
+      double time;
+      int code, lk;
+      PP_ROBOT_START();
+      scan_robot(cl[lane], sm.trf[lane], S, F, P, rk, &sm.cap[0][0], ri, max_steps, &time,
+                 &code, &lk);
+      // an open pair: NaN time (no result is NaN) and its next sample
+      sm.res_t[ri][lane] = lk < 0 ? time : CUDART_NAN;
+      sm.res_k[ri][lane] = lk < 0 ? code : lk;
+      PP_ROBOT_END(ri);
+    }
+    __syncthreads();
+    PP_TMARK(0);
+    if (kLeftovers) {
+      // rounds over the open pairs until none is left
+      const int n_pairs = F.n_scan * 32;
+      for (int round = 0;; ++round) {
+        if (threadIdx.x == 0) {
+          sm.n_left = 0;
+          sm.next_pair = 0;
+        }
+        __syncthreads();
+        for (int e0 = warp * 32; e0 < n_pairs; e0 += nwarps * 32) {
+          const int e = e0 + lane;
+          const bool open = e < n_pairs && isnan(sm.res_t[e >> 5][e & 31]);
+          const unsigned om = __ballot_sync(0xffffffffu, open);
+          if (om) {
+            unsigned at = 0;
+            if (lane == 0) at = atomicAdd(&sm.n_left, static_cast<unsigned>(__popc(om)));
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if (open) sm.left[at + __popc(om & ((1u << lane) - 1u))] = static_cast<uint16_t>(e);
+          }
+        }
+        __syncthreads();
+        const int n_left = static_cast<int>(sm.n_left);
+#ifdef PP_PHASE_CLOCKS
+        if (threadIdx.x == 0) sm.tph[3] = round == 0 ? n_left : sm.tph[3] + 10000;
+        if (threadIdx.x == 0 && blockIdx.x < kRecCtas && round < 8) {
+          g_round_rec[blockIdx.x][round][0] = n_left;
+          g_round_rec[blockIdx.x][round][1] = clock64();
+        }
+#endif
+        if (n_left == 0) break;
+        scan_leftovers(cl, sm.trf, sm.ke, sm.tile_uf, F, P, sm.rk, &sm.cap[0][0], sm.left, n_left,
+                       &sm.next_pair, sm.res_t, sm.res_k, P.scan_round_steps);
+        __syncthreads();
+      }
+    }
+    PP_TMARK(1);
+    PP_CMARK(0);
+
+    // ---- C: champions (dpps.cpp:140-213).  The update is a strict (time, id)
+    //      lexicographic argmin seeded with (kNever, -1), so visiting order
+    //      does not matter.  Feasible cells go to the frame's value queue.
+    if (warp == 0) {
+      const CellLane& c = reinterpret_cast<const CellLane*>(sm.cl_raw)[lane];
+      tile_champions<kCells>(
+          c, F, P, [&](int ri) { return sm.res_t[ri][lane]; },
+          [&](int ri) { return sm.res_k[ri][lane]; }, out, q, fc, f, kt, cell0);
+    }
+  }
+}
+
+template <bool kCells, int kWarps, int kCtas, bool kLeftovers = (kCtas <= 2)>
+__global__ void __launch_bounds__(kWarps * 32, kCtas)
+    scan_kernel(const FrameDev* __restrict__ frames, DevParams P, CellOut out, CellQueue q,
+                FrameCounters* __restrict__ fc, const __grid_constant__ FrameArg fa) {
+  __shared__ ScanSmem sm;
+  PP_CLOCK_INIT();
+  const int f = blockIdx.x / P.n_tiles;
+  const int tile = blockIdx.x % P.n_tiles;
+  // Let the value kernel (launched with programmatic stream serialization)
+  // get its CTAs resident while the last scan CTAs run; it waits for this
+  // grid's completion before reading anything (griddepcontrol.wait).
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (threadIdx.x == 0) atomicMax(&fc[f].t0_inv, ~pp_now_ns());
+  // warp 0's table rows (window phase) are requested before the frame
+  double4 dd = make_double4(0.0, 0.0, 0.0, 0.0);
+  PowRow pr{};
+  if (threadIdx.x < 32) {
+    const int kt = tile / (P.n_dirs * P.n_ptiles);
+    const int dir = (tile / P.n_ptiles) % P.n_dirs;
+    const int pw = (tile % P.n_ptiles) * 32 + threadIdx.x;
+    dd = P.dirs[dir];
+    pr = P.pows[kt * P.n_pows + (pw < P.n_pows ? pw : P.n_pows - 1)];
+  }
+#ifdef PP_PHASE_CLOCKS
+  if (threadIdx.x == 0 && blockIdx.x < kRecCtas) g_win_rec[blockIdx.x][3] = ph_last_;
+#endif
+  // (the frame is staged to shared memory inside scan_tile, overlapped with
+  // warp 0's windows, which read the few frame fields they need directly)
+  scan_tile<kCells, kLeftovers>(sm, P, out, q, fc, f, tile, dd, pr,
+                                P.frame_in_arg ? &fa.frame : frames + f,
+                                P.frame_in_arg ? fa.rk : nullptr);
+#ifdef PP_PHASE_CLOCKS
+  if (threadIdx.x == 0) {
+    const long long now_ = clock64();
+    ph_[0] = sm.tph[0] - ph_last_;       // window + lane-per-cell phase
+    ph_[1] = sm.tph[1] - sm.tph[0];      // leftovers
+    ph_[2] = now_ - sm.tph[1];           // champions + queue
+    ph_[3] = sm.tph[3];  // first-round open pairs + 10000 x rounds
+    ph_[4] = sm.tph[2] - ph_last_;       // window (A) alone
+  }
+#endif
+  PP_FLUSH(8);
+}
+
+// robot_consts of every scanned robot of every frame of a batch, once
+// (instead of once per tile): thread per (frame, robot).
+__global__ void __launch_bounds__(256) robot_consts_kernel(const FrameDev* __restrict__ frames,
+                                                           DevParams P, RobotK* __restrict__ out,
+                                                           int64_t n_frames) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t f = i / kMaxRobots;
+  const int ri = static_cast<int>(i % kMaxRobots);
+  if (f >= n_frames || ri >= frames[f].n_scan) return;
+  robot_consts(frames[f], P, ri, &out[i]);
+}
+
+}  // namespace pp
