@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(kThreads)
       volatile unsigned* fill = P.chunk_fill + ch;
       volatile unsigned* tiles = &fc[f].tiles_done;
       int nq = -1;
+      unsigned spins = 0;
       for (;;) {
         if (*fill == static_cast<unsigned>(kChunk)) break;
         if (*tiles == static_cast<unsigned>(P.n_tiles)) {
@@ -394,6 +395,7 @@ __global__ void __launch_bounds__(kThreads)
           break;
         }
         __nanosleep(256);
+        if (++spins > (1u << 26)) __trap();  // never: the scan grid always finishes
       }
       __threadfence();
       sm.n_act = nq;  // -1: a full chunk, the final count not known yet
@@ -421,7 +423,10 @@ __global__ void __launch_bounds__(kThreads)
       P.chunk_fill[ch] = 0;  // consumed (self-cleaning for the next launch)
       // the fold needs the final chunk count: wait for the scan's last tile
       volatile unsigned* tiles = &fc[f].tiles_done;
-      while (*tiles != static_cast<unsigned>(P.n_tiles)) __nanosleep(256);
+      for (unsigned spins = 0; *tiles != static_cast<unsigned>(P.n_tiles);) {
+        __nanosleep(256);
+        if (++spins > (1u << 26)) __trap();  // never: the scan grid always finishes
+      }
       __threadfence();
       const int nq = static_cast<int>(*reinterpret_cast<volatile unsigned*>(&fc[f].q_count));
       n_active = nq > 0 ? (nq + kChunk - 1) / kChunk : 1;
