@@ -295,14 +295,45 @@ pp_status pp_dpps_batch(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
                         const pp_params* params, const pp_search_grid* grid,
                         const int32_t* kicker_ids, pp_dpps_summary* summaries);
 
-/* Device-resident variant for benchmarking: frames already uploaded with
- * pp_batch_upload stay in HBM; pp_batch_run runs the search on them and
- * leaves summaries on the device until pp_batch_download. */
+/* Compact per-frame result of a batch (48 B): what log replay / what-if
+ * callers keep of each frame -- best_pass for all / flat / chip and the
+ * feasible counts (pass_eval.cpp:175-192, dpps.cpp:64-70). */
+typedef struct pp_frame_summary {
+  double best_score[3];   /* 0 when best_cell is -1 */
+  int32_t best_cell[3];   /* cell index (CandidateGrid order), -1 = nullopt */
+  int32_t n_feasible[3];  /* all / flat / chip */
+} pp_frame_summary;
+
+/* Batched frames end to end (the C5 log-replay path): the raw world states
+ * are copied to the device (one DMA; pinned memory from pp_host_alloc for
+ * full speed) and staged there -- teams id-sorted (dpps.cpp:79-92), the
+ * kicker chosen (kicker_ids[i], or the teammate nearest the ball when
+ * kicker_ids is NULL, ties to the earlier entry) -- then searched, scored
+ * and reduced on the device; one pp_frame_summary per frame comes back.
+ * PP_VALIDATION names the first frame whose kicker is not on team ours or
+ * whose team size is outside [0, 16] (the reference's run_dpps check,
+ * dpps.cpp:221-223).  Frames shard across devices by the caller. */
+pp_status pp_dpps_frames(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
+                         const pp_params* params, const pp_search_grid* grid,
+                         const int32_t* kicker_ids, pp_frame_summary* out);
+
+/* Device-resident pieces of pp_dpps_frames, for benchmarking and pipelined
+ * callers: pp_batch_upload copies the raw frames to HBM (asynchronously on
+ * the context's stream); pp_batch_run stages them and runs the search on the
+ * device, enqueued on the context's stream and NOT synchronised (device_ms,
+ * if non-NULL, synchronises and returns the device time of the run);
+ * pp_batch_download waits and copies the per-frame results back. */
 pp_status pp_batch_upload(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
                           const int32_t* kicker_ids);
 pp_status pp_batch_run(pp_ctx* ctx, const pp_params* params, const pp_search_grid* grid,
                        float* device_ms);
-pp_status pp_batch_download(pp_ctx* ctx, pp_dpps_summary* summaries);
+pp_status pp_batch_download(pp_ctx* ctx, pp_frame_summary* out);
+/* Kernels of the last pp_batch_run: number of pipeline launches and
+ * the summed device time of its scan and value kernels, measured on a
+ * re-run with events between the two (no overlap), `reps` times averaged. */
+pp_status pp_batch_kernel_times(pp_ctx* ctx, const pp_params* params, const pp_search_grid* grid,
+                                int32_t reps, float* stage_ms, float* scan_ms, float* value_ms,
+                                int32_t* n_scan_launches);
 
 /* ---- interception, possession, shot decision, free kick ----------------
  * (SURVEY §8(f) rows 2-4.)  One trajectory against robots, one warp per

@@ -102,6 +102,10 @@ class DppsSummary(C.Structure):
                 ("best_features", PassFeatures * 3), ("device_ms", _D)]
 
 
+class FrameSummary(C.Structure):  # pp_frame_summary (48 B per frame)
+    _fields_ = [("best_score", _D * 3), ("best_cell", _I * 3), ("n_feasible", _I * 3)]
+
+
 class RunFeatures(C.Structure):
     _fields_ = [(n, _D) for n in ("dist_to_goal", "dist_to_ball", "angle_to_goal", "guard_time",
                                   "defense_exposure")]
@@ -299,7 +303,12 @@ def _declare(lib):
                                   _P(C.c_int32), _P(DppsSummary)]
     lib.pp_batch_upload.argtypes = [vp, _P(World), C.c_int64, _P(C.c_int32)]
     lib.pp_batch_run.argtypes = [vp, _P(Params), _P(SearchGrid), _P(C.c_float)]
-    lib.pp_batch_download.argtypes = [vp, _P(DppsSummary)]
+    lib.pp_batch_download.argtypes = [vp, _P(FrameSummary)]
+    lib.pp_dpps_frames.argtypes = [vp, _P(World), C.c_int64, _P(Params), _P(SearchGrid),
+                                   _P(C.c_int32), _P(FrameSummary)]
+    fp = _P(C.c_float)
+    lib.pp_batch_kernel_times.argtypes = [vp, _P(Params), _P(SearchGrid), _I, fp, fp, fp,
+                                          _P(C.c_int32)]
     lib.pp_kick_trajectory.argtypes = [_P(Kick), _P(BallModel), _P(Trajectory), C.c_char_p,
                                        C.c_size_t]
     lib.pp_kick_trajectory.restype = C.c_int
@@ -311,7 +320,8 @@ def _declare(lib):
                                       _P(FreeKickPlan)]
     for fn in ("pp_params_validate", "pp_ctx_create", "pp_dpps", "pp_dpps_relaunch", "pp_score_cells",
                "pp_goal_views", "pp_runmap_count", "pp_runmap", "pp_dpps_batch",
-               "pp_batch_upload", "pp_batch_run", "pp_batch_download", "pp_intercept_all",
+               "pp_batch_upload", "pp_batch_run", "pp_batch_download", "pp_dpps_frames",
+               "pp_batch_kernel_times", "pp_intercept_all",
                "pp_possession", "pp_decide_shot", "pp_plan_free_kick"):
         getattr(lib, fn).restype = C.c_int
     return lib
@@ -339,7 +349,8 @@ EXPORTED_SYMBOLS = (
     "pp_dpps_upload_bytes", "pp_host_alloc",
     "pp_host_free", "pp_dpps", "pp_dpps_relaunch", "pp_ctx_stream", "pp_dpps_kernel_times",
     "pp_grid_cells", "pp_score_cells", "pp_goal_views", "pp_runmap",
-    "pp_dpps_batch", "pp_batch_upload", "pp_batch_run", "pp_batch_download",
+    "pp_dpps_batch", "pp_batch_upload", "pp_batch_run", "pp_batch_download", "pp_dpps_frames",
+    "pp_batch_kernel_times",
     "pp_score_running_points", "pp_kick_trajectory", "pp_intercept_all", "pp_possession",
     "pp_decide_shot", "pp_plan_free_kick",
 )

@@ -34,7 +34,9 @@ struct DevBuf {
   ~DevBuf() {
     if (p) cudaFree(p);
   }
-  cudaError_t reserve(size_t want) {
+  // Grow-only; new memory is zeroed on the context's stream `s`, so the
+  // kernels queued after it on that stream see the zeros.
+  cudaError_t reserve(cudaStream_t s, size_t want) {
     if (want <= bytes) return cudaSuccess;
     if (p) cudaFree(p);
     p = nullptr;
@@ -42,7 +44,7 @@ struct DevBuf {
     cudaError_t e = cudaMalloc(&p, want);
     if (e == cudaSuccess) {
       bytes = want;
-      e = cudaMemset(p, 0, want);
+      e = cudaMemsetAsync(p, 0, want, s);
     }
     return e;
   }
@@ -91,6 +93,11 @@ struct PipeRec {
 
 struct pp_ctx {
   int device = 0;
+  // Device shape, queried once: SM count and the resident CTAs per SM of the
+  // pipeline kernels (launch-shape thresholds derive from these, not from an
+  // assumed 148 SMs).
+  int n_sms = 0;
+  int occ_scan_wide = 0, occ_scan_mid = 0, occ_scan_narrow = 0, occ_value_wide = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evm = nullptr;
   // pp_dpps as one CUDA graph (scan, value; a D2H only for pageable
@@ -111,11 +118,14 @@ struct pp_ctx {
   std::vector<double> pows_key;  // inputs the power table was built from
   // run map
   DevBuf run_block, run_partials, run_counter;
-  // batch
-  DevBuf batch_frames, batch_sums, batch_rk;
-  std::vector<pp::FrameDev> batch_host;
-  std::vector<int32_t> batch_kickers, batch_poss;
+  // batch: raw worlds (+ caller's kicker ids) uploaded, staged FrameDevs,
+  // chosen kickers, first bad frame, robot constants, per-frame results
+  DevBuf batch_worlds, batch_kick_in, batch_frames, batch_kickers, batch_bad, batch_rk;
+  DevBuf batch_compact, batch_full;
   int64_t batch_n = 0;
+  int batch_max_scan = 1;      // widest scan list of the uploaded frames
+  bool batch_has_kickers = false;
+  bool batch_ran = false;
   // last single-frame launch (pp_dpps_relaunch)
   bool last_valid = false;
   pp::DevParams last_P{};
@@ -123,6 +133,21 @@ struct pp_ctx {
   pp_dpps_summary* last_dsum = nullptr;
   int last_threads = 0;
   std::unique_ptr<pp::FrameArg> last_fa{new pp::FrameArg()};  // the frame, as a parameter
+
+  pp_ctx() = default;
+  pp_ctx(const pp_ctx&) = delete;
+  pp_ctx& operator=(const pp_ctx&) = delete;
+  // Releases whatever a (possibly partial) pp_ctx_create acquired.
+  ~pp_ctx() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (evm) cudaEventDestroy(evm);
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
+    if (stream) cudaStreamDestroy(stream);
+  }
 };
 
 namespace {
@@ -146,6 +171,25 @@ pp_status fail(pp_ctx* ctx, pp_status st, const char* fmt, ...) {
     if (e_ != cudaSuccess)                                                                  \
       return fail((ctx), PP_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
                   __LINE__);                                                                \
+  } while (0)
+
+// Zero the pipeline's counters after a failed or stalled launch, so the
+// next call does not start from dirty queue bases (they are otherwise
+// self-cleaning, see FrameCounters).
+void reset_pipeline(pp_ctx* ctx) {
+  if (ctx->fcount.p) cudaMemsetAsync(ctx->fcount.p, 0, ctx->fcount.bytes, ctx->stream);
+  if (ctx->chunk_fill.p) cudaMemsetAsync(ctx->chunk_fill.p, 0, ctx->chunk_fill.bytes, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+}
+
+#define PP_PIPE_TRY(ctx, expr)                                                              \
+  do {                                                                                      \
+    const cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess) {                                                                \
+      reset_pipeline(ctx);                                                                  \
+      return fail((ctx), PP_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                                \
+    }                                                                                       \
   } while (0)
 
 void put(char* msg, size_t len, const std::string& s) {
@@ -479,9 +523,10 @@ cudaError_t ensure_tables(pp_ctx* ctx, pp::DevParams* P) {
       }
       d[i] = make_double4(dx.v, dy.v, ux.v, uy.v);
     }
-    e = ctx->dirs.reserve(d.size() * sizeof(double4));
+    e = ctx->dirs.reserve(ctx->stream, d.size() * sizeof(double4));
     if (e == cudaSuccess)
-      e = cudaMemcpy(ctx->dirs.p, d.data(), d.size() * sizeof(double4), cudaMemcpyHostToDevice);
+      e = cudaMemcpyAsync(ctx->dirs.p, d.data(), d.size() * sizeof(double4), cudaMemcpyHostToDevice,
+                          ctx->stream);
     if (e != cudaSuccess) return e;
     ctx->dirs_n = P->n_dirs;
     ctx->last_valid = false;
@@ -515,10 +560,10 @@ cudaError_t ensure_tables(pp_ctx* ctx, pp::DevParams* P) {
         }
       }
     }
-    e = ctx->pows.reserve(rows.size() * sizeof(pp::PowRow));
+    e = ctx->pows.reserve(ctx->stream, rows.size() * sizeof(pp::PowRow));
     if (e == cudaSuccess)
-      e = cudaMemcpy(ctx->pows.p, rows.data(), rows.size() * sizeof(pp::PowRow),
-                     cudaMemcpyHostToDevice);
+      e = cudaMemcpyAsync(ctx->pows.p, rows.data(), rows.size() * sizeof(pp::PowRow),
+                          cudaMemcpyHostToDevice, ctx->stream);
     if (e != cudaSuccess) return e;
     ctx->pows_key = key;
     ctx->last_valid = false;
@@ -526,6 +571,39 @@ cudaError_t ensure_tables(pp_ctx* ctx, pp::DevParams* P) {
   P->dirs = static_cast<const double4*>(ctx->dirs.p);
   P->pows = static_cast<const pp::PowRow*>(ctx->pows.p);
   return cudaSuccess;
+}
+
+// Resident CTAs per SM of the pipeline kernels (pp_ctx_create).
+cudaError_t query_occupancy(pp_ctx* ctx) {
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &ctx->occ_scan_wide, pp::scan_kernel<true, pp::kScanWarpsWide, pp::kScanCtasWide>,
+      32 * pp::kScanWarpsWide, 0);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &ctx->occ_scan_mid, pp::scan_kernel<true, pp::kScanWarpsMid, pp::kScanCtasMid, true>,
+        32 * pp::kScanWarpsMid, 0);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &ctx->occ_scan_narrow, pp::scan_kernel<true, pp::kScanWarpsNarrow, pp::kScanCtasNarrow>,
+        32 * pp::kScanWarpsNarrow, 0);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &ctx->occ_value_wide, pp::value_kernel<true, pp::kValueThreadsWide>,
+        pp::kValueThreadsWide, 0);
+  if (e == cudaSuccess && (ctx->occ_scan_wide < 1 || ctx->occ_scan_mid < 1 ||
+                           ctx->occ_scan_narrow < 1 || ctx->occ_value_wide < 1))
+    e = cudaErrorInvalidConfiguration;
+  return e;
+}
+
+// Largest value grid launched with the wide (single-frame, streaming) CTA
+// shape: up to 4 chunks per SM the 256-thread CTAs' shorter item chains pay
+// (measured: C1/C2 frames); beyond that the 128-thread shape packs better.
+// Correctness does not depend on residency: streaming CTAs only wait for scan
+// tiles, and every scan CTA has started before any value CTA runs (the scan
+// triggers griddepcontrol.launch_dependents first thing), so they all finish.
+int64_t value_wide_limit(const pp_ctx* ctx) {
+  return static_cast<int64_t>(ctx->n_sms) * std::max(ctx->occ_value_wide, 4);
 }
 
 // Robots scanned per tile (passed on as the scan CTA width request).
@@ -540,11 +618,11 @@ int64_t chunks_for(const pp::DevParams& P) {
 cudaError_t reserve_pipeline(pp_ctx* ctx, const pp::DevParams& P, int64_t n_frames) {
   const int64_t n_cells = static_cast<int64_t>(P.n_kt) * P.n_dirs * P.n_pows;
   const size_t n = static_cast<size_t>(n_frames * n_cells);
-  cudaError_t e = ctx->queue.reserve(n * (4 * sizeof(double) + sizeof(int32_t) + 1) + 64);
+  cudaError_t e = ctx->queue.reserve(ctx->stream, n * (4 * sizeof(double) + sizeof(int32_t) + 1) + 64);
   if (e != cudaSuccess) return e;
-  e = ctx->fcount.reserve(sizeof(pp::FrameCounters) * static_cast<size_t>(n_frames));
+  e = ctx->fcount.reserve(ctx->stream, sizeof(pp::FrameCounters) * static_cast<size_t>(n_frames));
   if (e != cudaSuccess) return e;
-  return ctx->partials.reserve(sizeof(pp::Partial) * static_cast<size_t>(n_frames * chunks_for(P)));
+  return ctx->partials.reserve(ctx->stream, sizeof(pp::Partial) * static_cast<size_t>(n_frames * chunks_for(P)));
 }
 
 
@@ -585,12 +663,13 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   }();
   ScanFn sfn;
   int w;
-  if (force_shape == 2 || (force_shape == 0 && ctas >= 2 * 148 * pp::kScanCtasNarrow)) {
+  const int64_t sms = ctx->n_sms;
+  if (force_shape == 2 || (force_shape == 0 && ctas >= 2 * sms * ctx->occ_scan_narrow)) {
     // Throughput (>= 2 waves of the narrow shape): 4-warp CTAs, 8 per SM,
     // robots round-robin over the warps.
     w = n_scan < pp::kScanWarpsNarrow ? n_scan : pp::kScanWarpsNarrow;
     sfn = pp::scan_kernel<kCells, pp::kScanWarpsNarrow, pp::kScanCtasNarrow>;
-  } else if (force_shape == 3 || (force_shape == 0 && ctas > 148 * pp::kScanCtasWide)) {
+  } else if (force_shape == 3 || (force_shape == 0 && ctas > sms * ctx->occ_scan_wide)) {
     // More tiles than one wave of the wide shape: 8-warp CTAs, 4 per SM
     // (one wave up to 592 tiles), robots two per warp, same leftover rounds.
     w = n_scan < pp::kScanWarpsMid ? n_scan : pp::kScanWarpsMid;
@@ -622,7 +701,7 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   cfg.attrs = attr;
   cfg.numAttrs = mid ? 0 : 1;  // (kernel timing splits the two grids)
   const int nch = static_cast<int>(chunks);
-  const bool wide = vctas <= 4u * 148u;
+  const bool wide = static_cast<int64_t>(vctas) <= value_wide_limit(ctx);
   const ValueFn vfn = wide ? pp::value_kernel<kCells, pp::kValueThreadsWide>
                            : pp::value_kernel<kCells, pp::kValueThreads>;
   cfg.blockDim = dim3(wide ? pp::kValueThreadsWide : pp::kValueThreads);
@@ -754,35 +833,30 @@ void pp_host_free(void* p) {
 pp_status pp_ctx_create(int device, pp_ctx** out) {
   if (!out) return PP_INTERNAL;
   *out = nullptr;
-  std::unique_ptr<pp_ctx> ctx(new pp_ctx());
-  ctx->device = device;
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device || device < 0)
     return PP_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return PP_CUDA;
+  // every early return below releases what was acquired (~pp_ctx)
+  std::unique_ptr<pp_ctx> ctx(new pp_ctx());
+  ctx->device = device;
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
     return PP_CUDA;
   if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
       cudaEventCreate(&ctx->evm) != cudaSuccess)
     return PP_CUDA;
-  if (ctx->frame.reserve(kFrameBytes) != cudaSuccess) return PP_CUDA;
+  if (cudaDeviceGetAttribute(&ctx->n_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+      ctx->n_sms < 1)
+    return PP_CUDA;
+  if (query_occupancy(ctx.get()) != cudaSuccess) return PP_CUDA;
+  if (ctx->frame.reserve(ctx->stream, kFrameBytes) != cudaSuccess) return PP_CUDA;
   if (ctx->frame_h.reserve(kFrameBytes) != cudaSuccess) return PP_CUDA;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return PP_CUDA;
   *out = ctx.release();
   return PP_OK;
 }
 
-void pp_ctx_destroy(pp_ctx* ctx) {
-  if (!ctx) return;
-  cudaSetDevice(ctx->device);
-  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
-  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
-  if (ctx->evm) cudaEventDestroy(ctx->evm);
-  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
-  if (ctx->graph) cudaGraphDestroy(ctx->graph);
-  if (ctx->stream) cudaStreamDestroy(ctx->stream);
-  delete ctx;
-}
+void pp_ctx_destroy(pp_ctx* ctx) { delete ctx; }
 
 const char* pp_last_error(const pp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
@@ -822,10 +896,10 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   std::memcpy(&fa->frame, F, sizeof(pp::FrameDev));
   for (int ri = 0; ri < F->n_scan; ++ri) pp::robot_consts(*F, P, ri, &fa->rk[ri]);
   P.frame_in_arg = 1;
-  PP_CUDA_TRY(ctx, ctx->block.reserve(off.total));
+  PP_CUDA_TRY(ctx, ctx->block.reserve(ctx->stream, off.total));
   PP_CUDA_TRY(ctx, reserve_pipeline(ctx, P, 1));
-  if (chunks_for(P) <= 4 * 148) {  // the value grid's wide (streaming) shape, see launch_pipeline
-    PP_CUDA_TRY(ctx, ctx->chunk_fill.reserve(sizeof(unsigned) * static_cast<size_t>(chunks_for(P))));
+  if (chunks_for(P) <= value_wide_limit(ctx)) {  // the value grid's wide (streaming) shape
+    PP_CUDA_TRY(ctx, ctx->chunk_fill.reserve(ctx->stream, sizeof(unsigned) * static_cast<size_t>(chunks_for(P))));
     P.chunk_fill = static_cast<unsigned*>(ctx->chunk_fill.p);
   }
   HT(2);
@@ -888,8 +962,10 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
     return e;
   };
   if (!pinned) {  // pageable block: plain stream work (graphs copy pinned memory only)
-    PP_CUDA_TRY(ctx, enqueue());
-    PP_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    // fold sentinel: the final fold overwrites device_ms (NaN bytes until then)
+    PP_PIPE_TRY(ctx, cudaMemsetAsync(&dsum->device_ms, 0xFF, sizeof(double), s));
+    PP_PIPE_TRY(ctx, enqueue());
+    PP_PIPE_TRY(ctx, cudaStreamSynchronize(s));
   } else {
   // The whole call is one graph: scan -> value (D2H only for pageable
   // blocks, which take the plain path above).
@@ -946,7 +1022,7 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
       }
       if (e == cudaSuccess && (!ctx->scan_node || !ctx->value_node)) e = cudaErrorInvalidValue;
     }
-    PP_CUDA_TRY(ctx, e);
+    PP_PIPE_TRY(ctx, e);
     ctx->gkey.assign(kb, kb + sizeof(key));
   } else {
     // same graph: only this frame's FrameArg changes
@@ -966,11 +1042,16 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
     PP_CUDA_TRY(ctx, cudaGraphExecKernelNodeSetParams(ctx->gexec, ctx->value_node, &kp));
   }
   HT(4);
-  PP_CUDA_TRY(ctx, cudaGraphLaunch(ctx->gexec, s));
-  PP_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  hv.summary->device_ms = std::numeric_limits<double>::quiet_NaN();  // fold sentinel
+  PP_PIPE_TRY(ctx, cudaGraphLaunch(ctx->gexec, s));
+  PP_PIPE_TRY(ctx, cudaStreamSynchronize(s));
   }
   HT(5);
   const double dms = hv.summary->device_ms;
+  if (std::isnan(dms)) {  // a streaming wait gave up: no fold ran
+    reset_pipeline(ctx);
+    return fail(ctx, PP_INTERNAL, "scan->value pipeline stalled (no fold); counters reset");
+  }
   fill_summary_host(hv.summary, *world, g, kicker_id, kicker_slot,
                     possession_of(*world, kicker_id, *params));
   hv.summary->device_ms = dms;
@@ -1007,8 +1088,8 @@ pp_status pp_score_cells(pp_ctx* ctx, const pp_world* world, const pp_params* pa
     in[4 * i + 2] = our_time[i];
     in[4 * i + 3] = opp_time[i];
   }
-  PP_CUDA_TRY(ctx, ctx->scratch_in.reserve(in.size() * 8));
-  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(6 * static_cast<size_t>(n) * 8));
+  PP_CUDA_TRY(ctx, ctx->scratch_in.reserve(ctx->stream, in.size() * 8));
+  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(ctx->stream, 6 * static_cast<size_t>(n) * 8));
   cudaStream_t s = ctx->stream;
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->frame.p, F, sizeof(pp::FrameDev), cudaMemcpyHostToDevice, s));
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->scratch_in.p, in.data(), in.size() * 8, cudaMemcpyHostToDevice, s));
@@ -1048,8 +1129,8 @@ pp_status pp_goal_views(pp_ctx* ctx, const pp_world* world, double robot_radius,
   std::vector<double> in(2 * static_cast<size_t>(n));
   std::memcpy(in.data(), px, n * 8);
   std::memcpy(in.data() + n, py, n * 8);
-  PP_CUDA_TRY(ctx, ctx->scratch_in.reserve(in.size() * 8));
-  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(4 * static_cast<size_t>(n) * 8));
+  PP_CUDA_TRY(ctx, ctx->scratch_in.reserve(ctx->stream, in.size() * 8));
+  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(ctx->stream, 4 * static_cast<size_t>(n) * 8));
   cudaStream_t s = ctx->stream;
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->frame.p, F, sizeof(pp::FrameDev), cudaMemcpyHostToDevice, s));
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->scratch_in.p, in.data(), in.size() * 8, cudaMemcpyHostToDevice, s));
@@ -1256,11 +1337,11 @@ pp_status pp_runmap(pp_ctx* ctx, const pp_world* world, const pp_params* params,
                 static_cast<long long>(block_vertices), static_cast<long long>(rs.n_map));
   PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   const pp_runmap_offsets_ off = pp_runmap_offsets_for_(n_map);
-  PP_CUDA_TRY(ctx, ctx->run_block.reserve(off.total));
+  PP_CUDA_TRY(ctx, ctx->run_block.reserve(ctx->stream, off.total));
   int max_blocks = 1;
   for (int z = 0; z < 4; ++z) max_blocks = std::max(max_blocks, rs.R.blocks_per_zone[z]);
-  PP_CUDA_TRY(ctx, ctx->run_partials.reserve(sizeof(pp::RunPartial) * 4 * max_blocks));
-  PP_CUDA_TRY(ctx, ctx->run_counter.reserve(sizeof(unsigned) * 4));  // done count, pad, u64 scorable
+  PP_CUDA_TRY(ctx, ctx->run_partials.reserve(ctx->stream, sizeof(pp::RunPartial) * 4 * max_blocks));
+  PP_CUDA_TRY(ctx, ctx->run_counter.reserve(ctx->stream, sizeof(unsigned) * 4));  // done count, pad, u64 scorable
   // (the map is written in device memory and copied in one DMA transfer:
   // tens of MB of per-thread stores straight into host memory are slower)
   char* d = static_cast<char*>(ctx->run_block.p);
@@ -1322,8 +1403,8 @@ pp_status pp_score_running_points(pp_ctx* ctx, const pp_world* world, const pp_p
   std::vector<double> in(2 * static_cast<size_t>(n));
   std::memcpy(in.data(), px, n * 8);
   std::memcpy(in.data() + n, py, n * 8);
-  PP_CUDA_TRY(ctx, ctx->scratch_in.reserve(in.size() * 8));
-  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(7 * static_cast<size_t>(n) * 8));
+  PP_CUDA_TRY(ctx, ctx->scratch_in.reserve(ctx->stream, in.size() * 8));
+  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(ctx->stream, 7 * static_cast<size_t>(n) * 8));
   cudaStream_t s = ctx->stream;
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->scratch_in.p, in.data(), in.size() * 8, cudaMemcpyHostToDevice, s));
   const double* d = static_cast<const double*>(ctx->scratch_in.p);
@@ -1344,45 +1425,88 @@ pp_status pp_score_running_points(pp_ctx* ctx, const pp_world* world, const pp_p
 }
 
 // ---------------------------------------------------------------------------
-// Batched frames: one CTA per frame, summaries only.
+// Batched frames (C5): raw worlds staged on the device, compact summaries.
 
-pp_status pp_batch_upload(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
-                          const int32_t* kicker_ids) {
-  if (!ctx || (!frames && n_frames > 0)) return fail(ctx, PP_INTERNAL, "null argument");
-  ctx->err.clear();
-  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-  ctx->batch_host.resize(static_cast<size_t>(n_frames));
-  ctx->batch_kickers.resize(static_cast<size_t>(n_frames));
-  for (int64_t i = 0; i < n_frames; ++i) {
-    const pp_world& w = frames[i];
-    int32_t kicker = -1;
-    if (kicker_ids) {
-      kicker = kicker_ids[i];
-    } else {  // nearest teammate, ties to the earlier entry
-      double best = std::numeric_limits<double>::infinity();
-      for (int r = 0; r < w.n_ours; ++r) {
-        const double d = host_distance(w.ours[r].px, w.ours[r].py, w.ball_px, w.ball_py);
-        if (d < best) {
-          best = d;
-          kicker = w.ours[r].id;
-        }
-      }
-    }
-    ctx->batch_kickers[i] = kicker;
-    int32_t ks = -1;
-    std::string why;
-    if (!pack_frame(w, kicker, &ctx->batch_host[i], &ks, &why))
-      return fail(ctx, PP_VALIDATION, "frame %lld: %s", static_cast<long long>(i), why.c_str());
+}  // extern "C"
+
+namespace {
+
+// Stage + robot constants + the search pipeline for the uploaded frames,
+// enqueued on the context's stream.  full != nullptr: full pp_dpps_summary
+// per frame (pp_dpps_batch), else the compact pp_frame_summary.  With
+// ev_stage / ev_scan / ev_value the pipeline runs group by group with
+// events between its kernels (kernel timing; no PDL overlap).
+struct BatchTimes {
+  double stage_ms = 0.0, scan_ms = 0.0, value_ms = 0.0;
+  int n_scan_launches = 0;
+};
+
+cudaError_t enqueue_batch(pp_ctx* ctx, pp::DevParams P, pp_dpps_summary* full,
+                          BatchTimes* times) {
+  const int64_t n = ctx->batch_n;
+  cudaStream_t s = ctx->stream;
+  const int64_t n_cells = static_cast<int64_t>(P.n_kt) * P.n_dirs * P.n_pows;
+  // Frames are independent: launch them in groups so the per-frame cell
+  // queues stay a bounded working set (group x cells x 37 B).
+  static const int64_t max_group = [] {
+    const char* e = getenv("PP_BATCH_GROUP");  // dev knob
+    return e ? std::max<int64_t>(1, atoll(e)) : int64_t(4096);
+  }();
+  int64_t group = (int64_t(1) << 28) / std::max<int64_t>(n_cells, 1);
+  group = std::max<int64_t>(1, std::min<int64_t>(group, std::min<int64_t>(n, max_group)));
+  cudaError_t e = reserve_pipeline(ctx, P, group);
+  if (e == cudaSuccess)
+    e = ctx->batch_rk.reserve(ctx->stream, sizeof(pp::RobotK) * pp::kMaxRobots * static_cast<size_t>(n));
+  if (e != cudaSuccess) return e;
+  auto* frames = static_cast<pp::FrameDev*>(ctx->batch_frames.p);
+  auto* rk = static_cast<pp::RobotK*>(ctx->batch_rk.p);
+  if (times) cudaEventRecord(ctx->ev0, s);
+  e = cudaMemsetAsync(ctx->batch_bad.p, 0xFF, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  pp::stage_frames_kernel<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, s>>>(
+      static_cast<const pp_world*>(ctx->batch_worlds.p),
+      ctx->batch_has_kickers ? static_cast<const int32_t*>(ctx->batch_kick_in.p) : nullptr, n,
+      frames, static_cast<int32_t*>(ctx->batch_kickers.p),
+      static_cast<unsigned long long*>(ctx->batch_bad.p));
+  // every frame's robot filter constants once, not once per tile
+  pp::robot_consts_kernel<<<static_cast<unsigned>((n * pp::kMaxRobots + 255) / 256), 256, 0, s>>>(
+      frames, P, rk, n);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (times) {
+    cudaEventRecord(ctx->ev1, s);
+    e = cudaEventSynchronize(ctx->ev1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    times->stage_ms += ms;
   }
-  ctx->batch_n = n_frames;
-  PP_CUDA_TRY(ctx, ctx->batch_frames.reserve(sizeof(pp::FrameDev) * std::max<int64_t>(n_frames, 1)));
-  PP_CUDA_TRY(ctx, cudaMemcpy(ctx->batch_frames.p, ctx->batch_host.data(),
-                              sizeof(pp::FrameDev) * n_frames, cudaMemcpyHostToDevice));
-  return PP_OK;
+  const int threads = 32 * warps_for(ctx->batch_max_scan);
+  pp::CellOut co{};
+  auto* compact = static_cast<pp_frame_summary*>(ctx->batch_compact.p);
+  for (int64_t f0 = 0; e == cudaSuccess && f0 < n; f0 += group) {
+    const int64_t nf = std::min(group, n - f0);
+    pp::DevParams Pg = P;
+    Pg.rk_pre = rk + f0 * pp::kMaxRobots;
+    Pg.compact = full ? nullptr : compact + f0;
+    if (times) cudaEventRecord(ctx->ev0, s);
+    e = launch_pipeline<false>(ctx, frames + f0, nf, Pg, threads, co, full ? full + f0 : nullptr,
+                               times ? ctx->evm : nullptr);
+    if (e == cudaSuccess && times) {
+      cudaEventRecord(ctx->ev1, s);
+      e = cudaEventSynchronize(ctx->ev1);
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, ctx->ev0, ctx->evm);
+      cudaEventElapsedTime(&b, ctx->evm, ctx->ev1);
+      times->scan_ms += a;
+      times->value_ms += b;
+      times->n_scan_launches += 1;
+    }
+  }
+  return e;
 }
 
-pp_status pp_batch_run(pp_ctx* ctx, const pp_params* params, const pp_search_grid* grid_in,
-                       float* device_ms) {
+pp_status batch_prepare(pp_ctx* ctx, const pp_params* params, const pp_search_grid* grid_in,
+                        pp::DevParams* P) {
   if (!ctx || !params) return fail(ctx, PP_INTERNAL, "null argument");
   ctx->err.clear();
   const pp_search_grid& g = grid_in ? *grid_in : params->grid;
@@ -1390,73 +1514,185 @@ pp_status pp_batch_run(pp_ctx* ctx, const pp_params* params, const pp_search_gri
   if (!validate_grid(g, &why)) return fail(ctx, PP_CONFIG, "%s", why.c_str());
   if (!validate_params(*params, &why)) return fail(ctx, PP_CONFIG, "%s", why.c_str());
   PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-  const int64_t n = ctx->batch_n;
-  PP_CUDA_TRY(ctx, ctx->batch_sums.reserve(sizeof(pp_dpps_summary) * std::max<int64_t>(n, 1)));
-  if (n == 0 || pp_grid_cells(&g) == 0) {
+  *P = make_dev_params(*params, g);
+  PP_CUDA_TRY(ctx, ensure_tables(ctx, P));
+  const size_t n = static_cast<size_t>(std::max<int64_t>(ctx->batch_n, 1));
+  PP_CUDA_TRY(ctx, ctx->batch_frames.reserve(ctx->stream, sizeof(pp::FrameDev) * n));
+  PP_CUDA_TRY(ctx, ctx->batch_kickers.reserve(ctx->stream, sizeof(int32_t) * n));
+  PP_CUDA_TRY(ctx, ctx->batch_bad.reserve(ctx->stream, sizeof(unsigned long long)));
+  PP_CUDA_TRY(ctx, ctx->batch_compact.reserve(ctx->stream, sizeof(pp_frame_summary) * n));
+  return PP_OK;
+}
+
+// The first frame the device could not stage, as the host's pack_frame
+// would have reported it.
+pp_status batch_check(pp_ctx* ctx) {
+  unsigned long long bad = ~0ull;
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(&bad, ctx->batch_bad.p, sizeof(bad), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+  PP_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (bad == ~0ull) return PP_OK;
+  const long long f = static_cast<long long>(bad >> 2);
+  if ((bad & 3ull) == pp::kStageTeamSize)
+    return fail(ctx, PP_VALIDATION, "frame %lld: team size outside [0, 16]", f);
+  int32_t kid = -1;
+  PP_CUDA_TRY(ctx, cudaMemcpy(&kid, static_cast<const int32_t*>(ctx->batch_kickers.p) + f,
+                              sizeof(kid), cudaMemcpyDeviceToHost));
+  return fail(ctx, PP_VALIDATION, "frame %lld: kicker id %d is not on team ours", f, kid);
+}
+
+}  // namespace
+
+extern "C" {
+
+pp_status pp_batch_upload(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
+                          const int32_t* kicker_ids) {
+  if (!ctx || (!frames && n_frames > 0) || n_frames < 0)
+    return fail(ctx, PP_INTERNAL, "null argument");
+  ctx->err.clear();
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  ctx->batch_ran = false;
+  ctx->batch_n = n_frames;
+  const size_t n = static_cast<size_t>(std::max<int64_t>(n_frames, 1));
+  PP_CUDA_TRY(ctx, ctx->batch_worlds.reserve(ctx->stream, sizeof(pp_world) * n));
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->batch_worlds.p, frames, sizeof(pp_world) * n_frames,
+                                   cudaMemcpyHostToDevice, ctx->stream));
+  ctx->batch_has_kickers = kicker_ids != nullptr;
+  if (kicker_ids) {
+    PP_CUDA_TRY(ctx, ctx->batch_kick_in.reserve(ctx->stream, sizeof(int32_t) * n));
+    PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->batch_kick_in.p, kicker_ids,
+                                     sizeof(int32_t) * n_frames, cudaMemcpyHostToDevice,
+                                     ctx->stream));
+  }
+  // widest scan list (the scan CTA's width request): ours minus the kicker
+  // plus theirs, from the team sizes alone
+  int widest = 1;
+  for (int64_t i = 0; i < n_frames; ++i) {
+    const int no = frames[i].n_ours, nt = frames[i].n_theirs;
+    if (no >= 0 && no <= PP_MAX_TEAM && nt >= 0 && nt <= PP_MAX_TEAM)
+      widest = std::max(widest, no - 1 + nt);
+  }
+  ctx->batch_max_scan = widest;
+  return PP_OK;
+}
+
+pp_status pp_batch_run(pp_ctx* ctx, const pp_params* params, const pp_search_grid* grid_in,
+                       float* device_ms) {
+  pp::DevParams P;
+  pp_status st = batch_prepare(ctx, params, grid_in, &P);
+  if (st != PP_OK) return st;
+  ctx->batch_ran = true;
+  if (ctx->batch_n == 0 || pp_grid_cells(grid_in ? grid_in : &params->grid) == 0) {
+    PP_CUDA_TRY(ctx, cudaMemsetAsync(ctx->batch_bad.p, 0xFF, sizeof(unsigned long long),
+                                     ctx->stream));
+    PP_CUDA_TRY(ctx, cudaMemsetAsync(ctx->batch_compact.p, 0,
+                                     sizeof(pp_frame_summary) * ctx->batch_n, ctx->stream));
     if (device_ms) *device_ms = 0.f;
     return PP_OK;
   }
-  pp::DevParams P = make_dev_params(*params, g);
-  PP_CUDA_TRY(ctx, ensure_tables(ctx, &P));
-  int max_scan = 0;
-  for (const auto& F : ctx->batch_host) max_scan = std::max(max_scan, F.n_scan);
-  const int threads = 32 * warps_for(max_scan);
-  cudaStream_t s = ctx->stream;
-  pp::CellOut co{};
-  // Frames are independent: launch them in groups so the per-frame cell
-  // queues stay a bounded working set (group x cells x 37 B).
-  const int64_t n_cells = pp_grid_cells(&g);
-  int64_t group = (int64_t(1) << 28) / std::max<int64_t>(n_cells, 1);
-  group = std::max<int64_t>(1, std::min<int64_t>(group, std::min<int64_t>(n, 4096)));
-  PP_CUDA_TRY(ctx, reserve_pipeline(ctx, P, group));
-  PP_CUDA_TRY(ctx, ctx->batch_rk.reserve(sizeof(pp::RobotK) * pp::kMaxRobots * static_cast<size_t>(n)));
-  const auto* frames = static_cast<const pp::FrameDev*>(ctx->batch_frames.p);
-  auto* rk = static_cast<pp::RobotK*>(ctx->batch_rk.p);
-  PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, s));
-  // every frame's robot filter constants once, not once per tile
-  pp::robot_consts_kernel<<<static_cast<unsigned>((n * pp::kMaxRobots + 255) / 256), 256, 0, s>>>(
-      frames, P, rk, n);
-  PP_CUDA_TRY(ctx, cudaGetLastError());
-  for (int64_t f0 = 0; f0 < n; f0 += group) {
-    const int64_t nf = std::min(group, n - f0);
-    pp::DevParams Pg = P;
-    Pg.rk_pre = rk + f0 * pp::kMaxRobots;
-    PP_CUDA_TRY(ctx, launch_pipeline<false>(ctx, frames + f0, nf, Pg, threads, co,
-                                            static_cast<pp_dpps_summary*>(ctx->batch_sums.p) + f0));
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (device_ms) {
+    PP_CUDA_TRY(ctx, cudaEventCreate(&t0));
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, ctx->stream);
   }
-  PP_CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, s));
-  PP_CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
-  if (device_ms) *device_ms = ms;
+  const cudaError_t e = enqueue_batch(ctx, P, nullptr, nullptr);
+  if (e != cudaSuccess) {
+    if (t0) cudaEventDestroy(t0);
+    if (t1) cudaEventDestroy(t1);
+    PP_PIPE_TRY(ctx, e);
+  }
+  if (device_ms) {
+    cudaEventRecord(t1, ctx->stream);
+    const cudaError_t e2 = cudaEventSynchronize(t1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    PP_PIPE_TRY(ctx, e2);
+    *device_ms = ms;
+  }
   return PP_OK;
 }
 
-pp_status pp_batch_download(pp_ctx* ctx, pp_dpps_summary* out) {
+pp_status pp_batch_download(pp_ctx* ctx, pp_frame_summary* out) {
   if (!ctx || (!out && ctx->batch_n > 0)) return fail(ctx, PP_INTERNAL, "null argument");
+  if (!ctx->batch_ran) return fail(ctx, PP_INTERNAL, "pp_batch_download before pp_batch_run");
   PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   const int64_t n = ctx->batch_n;
-  if (n == 0) return PP_OK;
-  PP_CUDA_TRY(ctx, cudaMemcpy(out, ctx->batch_sums.p, sizeof(pp_dpps_summary) * n,
-                              cudaMemcpyDeviceToHost));
+  if (n > 0)
+    PP_CUDA_TRY(ctx, cudaMemcpyAsync(out, ctx->batch_compact.p, sizeof(pp_frame_summary) * n,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+  return batch_check(ctx);
+}
+
+pp_status pp_batch_kernel_times(pp_ctx* ctx, const pp_params* params, const pp_search_grid* grid,
+                                int32_t reps, float* stage_ms, float* scan_ms, float* value_ms,
+                                int32_t* n_scan_launches) {
+  pp::DevParams P;
+  pp_status st = batch_prepare(ctx, params, grid, &P);
+  if (st != PP_OK) return st;
+  if (reps < 1 || ctx->batch_n == 0) return fail(ctx, PP_INTERNAL, "nothing to time");
+  BatchTimes t;
+  for (int r = 0; r < reps; ++r) PP_PIPE_TRY(ctx, enqueue_batch(ctx, P, nullptr, &t));
+  if (stage_ms) *stage_ms = static_cast<float>(t.stage_ms / reps);
+  if (scan_ms) *scan_ms = static_cast<float>(t.scan_ms / reps);
+  if (value_ms) *value_ms = static_cast<float>(t.value_ms / reps);
+  if (n_scan_launches) *n_scan_launches = t.n_scan_launches / reps;
   return PP_OK;
 }
 
+pp_status pp_dpps_frames(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
+                         const pp_params* params, const pp_search_grid* grid,
+                         const int32_t* kicker_ids, pp_frame_summary* out) {
+  pp_status st = pp_batch_upload(ctx, frames, n_frames, kicker_ids);
+  if (st == PP_OK) st = pp_batch_run(ctx, params, grid, nullptr);
+  if (st == PP_OK) st = pp_batch_download(ctx, out);
+  return st;
+}
+
+// Full per-frame summaries (the single-frame pp_dpps_summary, best features
+// included): the same device staging and search, then the host fills the
+// per-frame team tables.
 pp_status pp_dpps_batch(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
-                        const pp_params* params, const pp_search_grid* grid,
+                        const pp_params* params, const pp_search_grid* grid_in,
                         const int32_t* kicker_ids, pp_dpps_summary* summaries) {
+  if (!summaries && n_frames > 0) return fail(ctx, PP_INTERNAL, "null argument");
   pp_status st = pp_batch_upload(ctx, frames, n_frames, kicker_ids);
   if (st != PP_OK) return st;
-  st = pp_batch_run(ctx, params, grid, nullptr);
+  pp::DevParams P;
+  st = batch_prepare(ctx, params, grid_in, &P);
   if (st != PP_OK) return st;
-  st = pp_batch_download(ctx, summaries);
+  ctx->batch_ran = true;
+  const pp_search_grid& g = grid_in ? *grid_in : params->grid;
+  const size_t n = static_cast<size_t>(std::max<int64_t>(n_frames, 1));
+  PP_CUDA_TRY(ctx, ctx->batch_full.reserve(ctx->stream, sizeof(pp_dpps_summary) * n));
+  auto* full = static_cast<pp_dpps_summary*>(ctx->batch_full.p);
+  if (n_frames > 0 && pp_grid_cells(&g) > 0) {
+    PP_PIPE_TRY(ctx, enqueue_batch(ctx, P, full, nullptr));
+    PP_CUDA_TRY(ctx, cudaMemcpyAsync(summaries, full, sizeof(pp_dpps_summary) * n_frames,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+  } else {
+    PP_CUDA_TRY(ctx, cudaMemsetAsync(ctx->batch_bad.p, 0xFF, sizeof(unsigned long long),
+                                     ctx->stream));
+    std::memset(summaries, 0, sizeof(pp_dpps_summary) * static_cast<size_t>(n_frames));
+    for (int64_t i = 0; i < n_frames; ++i)
+      for (int k = 0; k < 3; ++k) summaries[i].best_cell[k] = -1;
+  }
+  std::vector<int32_t> kick(n);
+  if (n_frames > 0)
+    PP_CUDA_TRY(ctx, cudaMemcpyAsync(kick.data(), ctx->batch_kickers.p, sizeof(int32_t) * n_frames,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+  st = batch_check(ctx);  // (synchronises)
   if (st != PP_OK) return st;
-  const pp_search_grid& g = grid ? *grid : params->grid;
   for (int64_t i = 0; i < n_frames; ++i) {
-    const int32_t k = ctx->batch_kickers[i];
     const double dms = summaries[i].device_ms;
-    fill_summary_host(&summaries[i], frames[i], g, k, ctx->batch_host[i].kicker_slot,
-                      possession_of(frames[i], k, *params));
+    pp::FrameDev F;
+    int32_t ks = -1;
+    std::string why;
+    pack_frame(frames[i], kick[i], &F, &ks, &why);
+    fill_summary_host(&summaries[i], frames[i], g, kick[i], ks,
+                      possession_of(frames[i], kick[i], *params));
     summaries[i].device_ms = dms;
   }
   return PP_OK;
@@ -1517,7 +1753,7 @@ pp::BallPath path_of(const pp_trajectory& t) {
 cudaError_t run_intercepts(pp_ctx* ctx, const pp::FrameDev& F, const pp::DevParams& P,
                            const pp::BallPath& B, double dt, std::vector<pp::InterceptOut>* res) {
   cudaStream_t s = ctx->stream;
-  cudaError_t e = ctx->scratch_out.reserve(sizeof(pp::InterceptOut) * pp::kMaxRobots);
+  cudaError_t e = ctx->scratch_out.reserve(ctx->stream, sizeof(pp::InterceptOut) * pp::kMaxRobots);
   if (e != cudaSuccess) return e;
   e = cudaMemcpyAsync(ctx->frame.p, &F, sizeof(F), cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return e;
@@ -1665,7 +1901,7 @@ pp_status pp_decide_shot(pp_ctx* ctx, const pp_world* world, const pp_params* pa
   const double oy = has_ball ? world->ball_py : shooter->py;
   const pp::DevParams P = make_dev_params(*params, params->grid);
   cudaStream_t s = ctx->stream;
-  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(sizeof(pp_shot_decision)));
+  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(ctx->stream, sizeof(pp_shot_decision)));
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->frame.p, F, sizeof(*F), cudaMemcpyHostToDevice, s));
   pp::shot_kernel<<<1, 32 * std::max(F->n_scan, 2), 0, s>>>(
       static_cast<const pp::FrameDev*>(ctx->frame.p), P, ox, oy, shot_speed,

@@ -54,6 +54,9 @@ struct DevParams {
   // kernels' FrameArg parameter (no copy: the call graph updates the kernel
   // nodes' parameters), 0: from `frames` / rk_pre in global memory.
   int32_t frame_in_arg, pad3;
+  // Batches: the frame fold writes this compact per-frame result (indexed
+  // like the launch's frames) instead of the full pp_dpps_summary.
+  pp_frame_summary* compact;
 };
 
 // resolve_kick(power_table[p], kick type) and its sample counts, computed on

@@ -26,6 +26,9 @@ constexpr int kScanWarpsMid = 8, kScanCtasMid = 4;  // one wave of up to 4 x 148
 #define PP_VALUE_THREADS 128
 #endif
 constexpr int kChunk = PP_VALUE_CHUNK;           // queued cells per value CTA
+// A warp appends at most 32 queue entries, so they touch at most two chunks
+// (tile_champions' chunk_fill split), and D3 runs one cell per lane of warp 0.
+static_assert(kChunk == 32, "value chunks are one warp wide");
 constexpr int kMaxWarps = 16;                    // largest CTA of any pipeline kernel
 constexpr int kValueThreads = PP_VALUE_THREADS;  // threads per value CTA (pair/edge items) ...
 constexpr int kValueThreadsWide = 256;           // ... and for launches of at most a wave
@@ -33,15 +36,23 @@ constexpr int kIvCap = 8 * kChunk;               // blocking-opponent intervals 
 constexpr int kMaxHeights = 129;                 // view heights cached in shared memory
 constexpr int kMaxTeamIv = 16;                  // at most one interval per opponent
 
-// Per-frame counters, zeroed by the value kernel's last CTA (self-cleaning).
+// Per-frame counters, self-cleaning: the frame fold (last active value CTA)
+// zeroes q_count / n_feas / chunks_done / t0_inv; in streaming launches the
+// last value CTA of the frame to LEAVE (idle chunks included) zeroes
+// tiles_done / value_out, so no CTA still polling tiles_done can see it reset.
 struct FrameCounters {
   unsigned q_count;     // feasible cells queued
   unsigned n_feas[2];   // per kick slot
   unsigned chunks_done;
   unsigned tiles_done;  // scan tiles whose queue entries are written (streaming value)
-  unsigned pad;
+  unsigned value_out;   // streaming: value CTAs of the frame that have left
   unsigned long long t0_inv;  // ~(earliest scan CTA start, globaltimer ns); 0 = none
 };
+
+// Streaming waits give up after this many polls (~4 s): the CTA leaves
+// without folding, the host sees the fold missing, reports PP_INTERNAL and
+// zeroes the counters (no __trap: the context stays usable).
+constexpr unsigned kSpinLimit = 1u << 24;
 
 __device__ __forceinline__ unsigned long long pp_now_ns() {
   unsigned long long t;
@@ -164,6 +175,33 @@ __device__ void write_summary(pp_dpps_summary* S, const Partial& B, const DevPar
       S->best_features[0] = S->best_features[row];
     }
   }
+}
+
+// The compact per-frame result of a batch (pp_frame_summary).
+__device__ void write_compact(pp_frame_summary* C, const Partial& B, const DevParams& P) {
+  pp_frame_summary o;
+  for (int k = 0; k < 3; ++k) {
+    o.best_cell[k] = -1;
+    o.best_score[k] = 0.0;
+    o.n_feasible[k] = 0;
+  }
+  int64_t c0 = -1;
+  double s0 = 0.0;
+  for (int s = 0; s < P.n_kt; ++s) {
+    const int row = (s == 0 ? P.kt_chip0 : P.kt_chip1) ? 2 : 1;
+    o.n_feasible[row] = static_cast<int32_t>(B.n_feasible[s]);
+    o.n_feasible[0] += static_cast<int32_t>(B.n_feasible[s]);
+    if (B.cell[s] < 0) continue;
+    o.best_cell[row] = static_cast<int32_t>(B.cell[s]);
+    o.best_score[row] = B.score[s];
+    if (better(B.score[s], B.cell[s], s0, c0)) {
+      c0 = B.cell[s];
+      s0 = B.score[s];
+    }
+  }
+  o.best_cell[0] = static_cast<int32_t>(c0);
+  o.best_score[0] = s0;
+  *C = o;
 }
 
 // Optional per-phase cycle accounting (build with -DPP_PHASE_CLOCKS).
@@ -767,8 +805,11 @@ __device__ __forceinline__ void tile_champions(const CellLane& c, const FrameDev
       }
       base = __shfl_sync(0xffffffffu, base, 0);
       const unsigned n_new = static_cast<unsigned>(__popc(fm));
-      if (feas) {
-        const int64_t pos = static_cast<int64_t>(f) * q.cap + base + __popc(fm & ((1u << lane) - 1u));
+      const unsigned rank = __popc(fm & ((1u << lane) - 1u));
+      // (base + rank < cap always: a frame queues at most its cells; the
+      // guard keeps dirty counters from writing past the frame's region)
+      if (feas && base + rank < static_cast<unsigned>(q.cap)) {
+        const int64_t pos = static_cast<int64_t>(f) * q.cap + base + rank;
         q.rx[pos] = rx.v;
         q.ry[pos] = ry.v;
         q.ot[pos] = bt_o.v;

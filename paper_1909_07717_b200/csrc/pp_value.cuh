@@ -283,7 +283,7 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
 // fold order cannot change the winner.  Resets the frame's counters.
 __device__ __forceinline__ void fold_frame(FoldSmem& fs, const Partial* base, int n,
                                            FrameCounters* fcf, const DevParams& P,
-                                           pp_dpps_summary* S) {
+                                           pp_dpps_summary* S, int f) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
@@ -339,15 +339,18 @@ __device__ __forceinline__ void fold_frame(FoldSmem& fs, const Partial* base, in
       }
       acc.n_feasible[s] = fcf->n_feas[s];
     }
-    write_summary(S, acc, P);
-    // kernel span of this frame: first scan CTA start -> this fold
-    S->device_ms = fcf->t0_inv ? static_cast<double>(pp_now_ns() - ~fcf->t0_inv) * 1e-6 : 0.0;
+    if (P.compact) {
+      write_compact(P.compact + f, acc, P);
+    } else {
+      write_summary(S, acc, P);
+      // kernel span of this frame: first scan CTA start -> this fold
+      S->device_ms = fcf->t0_inv ? static_cast<double>(pp_now_ns() - ~fcf->t0_inv) * 1e-6 : 0.0;
+    }
     fcf->t0_inv = 0ull;
     fcf->q_count = 0;  // self-cleaning for the next launch / graph replay
     fcf->n_feas[0] = 0;
     fcf->n_feas[1] = 0;
     fcf->chunks_done = 0;
-    fcf->tiles_done = 0;
   }
 }
 
@@ -377,6 +380,17 @@ __global__ void __launch_bounds__(kThreads)
     value_heights(sm, P);
   }
   const bool stream = kEarly && P.chunk_fill != nullptr;
+  // Streaming: every value CTA of the frame counts itself out when it leaves;
+  // the last one zeroes the streaming counters (see FrameCounters).
+  auto leave = [&]() {
+    if (stream && threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(&fc[f].value_out, 1u) == static_cast<unsigned>(chunks_per_frame - 1)) {
+        fc[f].tiles_done = 0;
+        fc[f].value_out = 0;
+      }
+    }
+  };
   int n_q;
   if (stream) {
     // Scan -> value streaming (single frame): start as soon as this chunk's
@@ -386,28 +400,34 @@ __global__ void __launch_bounds__(kThreads)
       volatile unsigned* fill = P.chunk_fill + ch;
       volatile unsigned* tiles = &fc[f].tiles_done;
       int nq = -1;
-      unsigned spins = 0;
-      for (;;) {
+      for (unsigned spins = 0;; ++spins) {
         if (*fill == static_cast<unsigned>(kChunk)) break;
         if (*tiles == static_cast<unsigned>(P.n_tiles)) {
           __threadfence();
           nq = static_cast<int>(*reinterpret_cast<volatile unsigned*>(&fc[f].q_count));
           break;
         }
+        if (spins > kSpinLimit) {
+          nq = -2;  // stalled pipeline: leave without folding
+          break;
+        }
         __nanosleep(256);
-        if (++spins > (1u << 26)) __trap();  // never: the scan grid always finishes
       }
       __threadfence();
       sm.n_act = nq;  // -1: a full chunk, the final count not known yet
     }
     __syncthreads();
+    if (sm.n_act == -2) return;
     n_q = sm.n_act < 0 ? (ch + 1) * kChunk : sm.n_act;
   } else {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // scan grid done and visible
     n_q = static_cast<int>(fc[f].q_count);
   }
   const int n_active_lb = n_q > 0 ? (n_q + kChunk - 1) / kChunk : 1;
-  if (ch >= n_active_lb) return;
+  if (ch >= n_active_lb) {
+    leave();
+    return;
+  }
   if (!kEarly) {
     load_frame(&sm.frame, P.frame_in_arg ? &fa : frames + f);
     __syncthreads();
@@ -419,26 +439,35 @@ __global__ void __launch_bounds__(kThreads)
   value_chunk<kCells>(sm, P, q, out, f, e0, m, base + ch);
   if (threadIdx.x == 0) {
     int n_active = n_active_lb;
+    bool stalled = false;
     if (stream) {
       P.chunk_fill[ch] = 0;  // consumed (self-cleaning for the next launch)
       // the fold needs the final chunk count: wait for the scan's last tile
       volatile unsigned* tiles = &fc[f].tiles_done;
-      for (unsigned spins = 0; *tiles != static_cast<unsigned>(P.n_tiles);) {
+      for (unsigned spins = 0; *tiles != static_cast<unsigned>(P.n_tiles); ++spins) {
+        if (spins > kSpinLimit) {
+          stalled = true;
+          break;
+        }
         __nanosleep(256);
-        if (++spins > (1u << 26)) __trap();  // never: the scan grid always finishes
       }
       __threadfence();
       const int nq = static_cast<int>(*reinterpret_cast<volatile unsigned*>(&fc[f].q_count));
       n_active = nq > 0 ? (nq + kChunk - 1) / kChunk : 1;
     }
-    __threadfence();
-    const unsigned prev = atomicAdd(&fc[f].chunks_done, 1u);
-    sm.last = prev == static_cast<unsigned>(n_active - 1);
-    sm.n_act = n_active;
+    sm.last = 0;
+    sm.n_act = -2;
+    if (!stalled) {
+      __threadfence();
+      const unsigned prev = atomicAdd(&fc[f].chunks_done, 1u);
+      sm.last = prev == static_cast<unsigned>(n_active - 1);
+      sm.n_act = n_active;
+    }
   }
   __syncthreads();
-  if (!sm.last) return;
-  fold_frame(fs, base, sm.n_act, fc + f, P, summaries + f);
+  if (sm.n_act == -2) return;  // stalled: no fold (the host reports it)
+  if (sm.last) fold_frame(fs, base, sm.n_act, fc + f, P, summaries ? summaries + f : nullptr, f);
+  leave();  // after the fold: the fold reads the frame's counters
 }
 
 }  // namespace pp

@@ -45,7 +45,8 @@ def test_library_is_sm100a():
 STRUCTS = {"pp_world": abi.World, "pp_params": abi.Params, "pp_search_grid": abi.SearchGrid,
            "pp_dpps_summary": abi.DppsSummary, "pp_runmap_summary": abi.RunmapSummary,
            "pp_runmap_request": abi.RunmapRequest, "pp_pass_features": abi.PassFeatures,
-           "pp_robot": abi.Robot, "pp_thresholds": abi.Thresholds}
+           "pp_robot": abi.Robot, "pp_thresholds": abi.Thresholds,
+           "pp_frame_summary": abi.FrameSummary}
 
 
 def test_struct_layouts_match_header(tmp_path):

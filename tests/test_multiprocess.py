@@ -1,7 +1,8 @@
 """CPU, world_size 2 over gloo: the multi-GPU host path for batched frames
 (contiguous frame shards, no collective inside a frame, final gather on rank
 0) reproduces a single-process run bit for bit.  The per-rank runner is the
-CPU oracle here; on GPUs it is pp_dpps_batch (tests/test_gpu_batch.py)."""
+CPU oracle here; on GPUs it is pp_dpps_frames (tests/test_gpu_batch.py,
+test_run_sharded_product_runner_n1)."""
 import ctypes as C
 import os
 import socket
@@ -19,10 +20,9 @@ GRID = abi.SearchGrid(12, 6, 1.0, 6.5, 1, 1)
 
 
 def _frames(n):
-    import sys
-    sys.path.insert(0, ROOT)
-    from bench import synthetic_frames
-    return synthetic_frames(n, seed=123)
+    from paper_1909_07717_b200 import synthetic
+    arr, keep = synthetic.as_ctypes(synthetic.c5_frames(0, n))
+    return list(arr)
 
 
 def _oracle_runner(frames):
