@@ -226,6 +226,16 @@ typedef struct pp_ctx pp_ctx;
 
 pp_status pp_ctx_create(int device, pp_ctx** out);
 void pp_ctx_destroy(pp_ctx* ctx);
+/* Context options.  PP_OPT_EXACT_ONLY (value 1 = on): verification switch
+ * that turns off every FP32 shortcut of the kernels -- the reach / arrival
+ * lower-bound rejects, skip-ahead, upper-bound accepts and window prunes of
+ * the scan and interception kernels, and the FP32 gate / geometric band of
+ * goal_view -- so every in-window sample and every bisection step takes the
+ * reference's exact FP64 test (kernel.hpp:33-44, pass_eval.cpp:15-51).
+ * Results must be byte-identical either way; only speed differs.  The
+ * environment variable PP_EXACT_ONLY=1 sets it at pp_ctx_create. */
+#define PP_OPT_EXACT_ONLY 1
+pp_status pp_ctx_set_option(pp_ctx* ctx, int32_t option, int32_t value);
 /* Message of the last failing call on this context (valid until the next call). */
 const char* pp_last_error(const pp_ctx* ctx);
 /* KernelBackend::name equivalent (kernel.hpp:50-53): "sm100a". */

@@ -17,6 +17,7 @@ STATUS_NAMES = {0: "ok", 1: "schema", 2: "validation", 3: "config", 4: "domain",
                 5: "internal", 6: "cuda"}
 PP_COPY_SUMMARY = 0
 PP_COPY_ALL = 1
+PP_OPT_EXACT_ONLY = 1
 
 _D = C.c_double
 _I = C.c_int32
@@ -273,6 +274,8 @@ def _declare(lib):
     lib.pp_grid_cells.argtypes = [_P(SearchGrid)]
     lib.pp_grid_cells.restype = C.c_int64
     lib.pp_ctx_create.argtypes = [C.c_int, _P(vp)]
+    lib.pp_ctx_set_option.argtypes = [vp, _I, _I]
+    lib.pp_ctx_set_option.restype = C.c_int
     lib.pp_ctx_destroy.argtypes = [vp]
     lib.pp_ctx_destroy.restype = None
     lib.pp_last_error.argtypes = [vp]
@@ -345,7 +348,7 @@ def load_library(path: str = LIB_PATH):
 EXPORTED_SYMBOLS = (
     "pp_params_default", "pp_params_validate", "pp_grid_bytes", "pp_grid_view_of",
     "pp_runmap_bytes", "pp_runmap_view_of", "pp_runmap_count", "pp_ctx_create",
-    "pp_ctx_destroy", "pp_last_error", "pp_kernel_name", "pp_abi_version",
+    "pp_ctx_destroy", "pp_ctx_set_option", "pp_last_error", "pp_kernel_name", "pp_abi_version",
     "pp_dpps_upload_bytes", "pp_host_alloc",
     "pp_host_free", "pp_dpps", "pp_dpps_relaunch", "pp_ctx_stream", "pp_dpps_kernel_times",
     "pp_grid_cells", "pp_score_cells", "pp_goal_views", "pp_runmap",

@@ -98,6 +98,8 @@ struct pp_ctx {
   // assumed 148 SMs).
   int n_sms = 0;
   int occ_scan_wide = 0, occ_scan_mid = 0, occ_scan_narrow = 0, occ_value_wide = 0;
+  // PP_OPT_EXACT_ONLY: every FP32 filter off (verification switch)
+  int exact_only = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evm = nullptr;
   // pp_dpps as one CUDA graph (scan, value; a D2H only for pageable
@@ -415,8 +417,9 @@ double sqrt_le_threshold(double m) {
   return x;
 }
 
-pp::DevParams make_dev_params(const pp_params& p, const pp_search_grid& g) {
+pp::DevParams make_dev_params(const pp_ctx* ctx, const pp_params& p, const pp_search_grid& g) {
   pp::DevParams d{};
+  d.exact_only = ctx->exact_only;
   d.r_lt2 = sqrt_lt_threshold(p.thresholds.robot_radius);
   d.mb_le2 = sqrt_le_threshold(p.thresholds.robot_radius + 1e-9);
   d.slide = p.ball.slide_decel;
@@ -852,11 +855,24 @@ pp_status pp_ctx_create(int device, pp_ctx** out) {
   if (ctx->frame.reserve(ctx->stream, kFrameBytes) != cudaSuccess) return PP_CUDA;
   if (ctx->frame_h.reserve(kFrameBytes) != cudaSuccess) return PP_CUDA;
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return PP_CUDA;
+  if (const char* e = std::getenv("PP_EXACT_ONLY")) ctx->exact_only = std::atoi(e) != 0;
   *out = ctx.release();
   return PP_OK;
 }
 
 void pp_ctx_destroy(pp_ctx* ctx) { delete ctx; }
+
+pp_status pp_ctx_set_option(pp_ctx* ctx, int32_t option, int32_t value) {
+  if (!ctx) return PP_INTERNAL;
+  switch (option) {
+    case PP_OPT_EXACT_ONLY:
+      ctx->exact_only = value != 0;
+      ctx->last_valid = false;  // (pp_dpps_relaunch would replay the old setting)
+      return PP_OK;
+    default:
+      return fail(ctx, PP_CONFIG, "unknown context option %d", option);
+  }
+}
 
 const char* pp_last_error(const pp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
@@ -888,7 +904,7 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
                       possession_of(*world, kicker_id, *params));
     return PP_OK;
   }
-  pp::DevParams P = make_dev_params(*params, g);
+  pp::DevParams P = make_dev_params(ctx, *params, g);
   PP_CUDA_TRY(ctx, ensure_tables(ctx, &P));
   // The frame and its robots' filter constants (computed here once, not per
   // tile) travel in the kernels' FrameArg parameter: no host-to-device copy.
@@ -1080,7 +1096,7 @@ pp_status pp_score_cells(pp_ctx* ctx, const pp_world* world, const pp_params* pa
     w.ours[0] = pp_robot{0, 0, 0, 0, 0, 0, 0};
   }
   if (!pack_frame(w, w.ours[0].id, F, &ks, &why)) return fail(ctx, PP_VALIDATION, "%s", why.c_str());
-  const pp::DevParams P = make_dev_params(*params, params->grid);
+  const pp::DevParams P = make_dev_params(ctx, *params, params->grid);
   std::vector<double> in(4 * static_cast<size_t>(n));
   for (int64_t i = 0; i < n; ++i) {
     in[4 * i] = rx[i];
@@ -1138,7 +1154,7 @@ pp_status pp_goal_views(pp_ctx* ctx, const pp_world* world, double robot_radius,
   pp::goal_view_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(
       static_cast<const pp::FrameDev*>(ctx->frame.p), robot_radius,
       sqrt_lt_threshold(robot_radius), sqrt_le_threshold(robot_radius + 1e-9), n, dpx, dpx + n,
-      static_cast<double*>(ctx->scratch_out.p));
+      static_cast<double*>(ctx->scratch_out.p), ctx->exact_only != 0);
   PP_CUDA_TRY(ctx, cudaGetLastError());
   std::vector<double> o(4 * static_cast<size_t>(n));
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(o.data(), ctx->scratch_out.p, o.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -1514,7 +1530,7 @@ pp_status batch_prepare(pp_ctx* ctx, const pp_params* params, const pp_search_gr
   if (!validate_grid(g, &why)) return fail(ctx, PP_CONFIG, "%s", why.c_str());
   if (!validate_params(*params, &why)) return fail(ctx, PP_CONFIG, "%s", why.c_str());
   PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-  *P = make_dev_params(*params, g);
+  *P = make_dev_params(ctx, *params, g);
   PP_CUDA_TRY(ctx, ensure_tables(ctx, P));
   const size_t n = static_cast<size_t>(std::max<int64_t>(ctx->batch_n, 1));
   PP_CUDA_TRY(ctx, ctx->batch_frames.reserve(ctx->stream, sizeof(pp::FrameDev) * n));
@@ -1823,7 +1839,7 @@ pp_status pp_intercept_all(pp_ctx* ctx, const pp_world* world, const pp_params* 
   int32_t ks = -1;
   if (!pack_frame(*world, -1, F, &ks, &why, ScanList::kAll))
     return fail(ctx, PP_VALIDATION, "%s", why.c_str());
-  const pp::DevParams P = make_dev_params(*params, params->grid);
+  const pp::DevParams P = make_dev_params(ctx, *params, params->grid);
   std::vector<pp::InterceptOut> res;
   PP_CUDA_TRY(ctx, run_intercepts(ctx, *F, P, B, dt, &res));
   for (int i = 0; i < F->n_scan; ++i) {
@@ -1899,7 +1915,7 @@ pp_status pp_decide_shot(pp_ctx* ctx, const pp_world* world, const pp_params* pa
                         params->thresholds.possession_radius;
   const double ox = has_ball ? world->ball_px : shooter->px;
   const double oy = has_ball ? world->ball_py : shooter->py;
-  const pp::DevParams P = make_dev_params(*params, params->grid);
+  const pp::DevParams P = make_dev_params(ctx, *params, params->grid);
   cudaStream_t s = ctx->stream;
   PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(ctx->stream, sizeof(pp_shot_decision)));
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->frame.p, F, sizeof(*F), cudaMemcpyHostToDevice, s));

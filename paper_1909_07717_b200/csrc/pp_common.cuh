@@ -38,7 +38,12 @@ struct DevParams {
   int32_t n_dirs, n_pows, n_kt, kt_chip0, kt_chip1, n_ptiles, n_tiles;
   // leftover rounds (16- and 8-warp scan shapes): lane-per-cell steps before
   // a (robot, cell) goes to scan_leftovers, and its steps per round there
-  int32_t scan_steps, scan_round_steps, pad;
+  int32_t scan_steps, scan_round_steps;
+  // Verification switch (pp_ctx_set_option PP_OPT_EXACT_ONLY): every FP32
+  // filter passes through -- no reach / lower-bound rejects, no skip-ahead,
+  // no upper-bound accepts, no FP32 window prunes, no FP32 / band shortcuts
+  // in goal_view -- so every in-window sample takes the exact FP64 test.
+  int32_t exact_only;
   // World-independent tables built on the host (pp_cabi.cu ensure_tables):
   const double4* dirs;      // [n_dirs] raw (x, y) and unit (x, y), dpps.cpp:37-48, 120-122
   const struct PowRow* pows;  // [n_kt][n_pows] trajectory per kick slot and power

@@ -120,7 +120,9 @@ __device__ __forceinline__ InterceptOut intercept_warp(const BallPath& B, int kb
     // 1 window end, 2 certainly feasible, 3 needs the exact test.
     const int kk = k0 + lane;
     int code = 1, nx = kk + 1;
-    if (kk < ke) {
+    if (kk < ke && P.exact_only) {
+      code = 3;  // verification switch: the exact test for every sample
+    } else if (kk < ke) {
       const float tf = static_cast<float>(kk) * dtf;
       const float sf = trf.distance_at(tf);
       const float qxf = fmaf(uxf, sf, bxf);
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(512) shot_kernel(const FrameDev* __restrict__ 
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    view = goal_view_thread(ox, oy, F, P.radius, P.r_lt2, P.mb_le2);
+    view = goal_view_thread(ox, oy, F, P.radius, P.r_lt2, P.mb_le2, P.exact_only != 0);
     const xd gx = xd(0.5) * xd(F.L);
     pp_shot_decision d{};
     d.shot_angle = view.angle;

@@ -410,6 +410,7 @@ struct SampleF {
   float uxf, uyf;       // the tile's direction
   float dtf, radf;
   float s0;             // ray coordinate of the robot's closest approach
+  bool exact;           // DevParams::exact_only: no filtering at all
 };
 
 __device__ __forceinline__ SampleF sample_f(const RobotK& rk, float2 uf, const DevParams& P) {
@@ -422,6 +423,7 @@ __device__ __forceinline__ SampleF sample_f(const RobotK& rk, float2 uf, const D
   S.dtf = P.dtf;
   S.radf = P.radf;
   S.s0 = -(S.bxf * S.uxf + S.byf * S.uyf);
+  S.exact = P.exact_only != 0;
   return S;
 }
 
@@ -433,6 +435,7 @@ __device__ __forceinline__ int test_sample(const RobotK& rk, const SampleF& S, i
                                            const TrajF& tf_, int ke_s, int cap_c, int* next) {
   if (kk >= ke_s) return kEnd;
   if (kk > cap_c) return kCap;
+  if (S.exact) return kCand;
   const float tf = static_cast<float>(kk) * S.dtf;
   const float sf = tf_.distance_at(tf);
   const float qxf = fmaf(S.uxf, sf, S.bxf);
@@ -548,7 +551,9 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
   const int kb = c.kb;
   const int ke = valid ? c.ke : 0;
   int k = ke;
-  if (valid && kb < ke) {
+  if (valid && kb < ke && S.exact) {
+    k = kb;  // no FP32 prunes: every in-window sample is tested
+  } else if (valid && kb < ke) {
     // scan_robot's prunes (intercept.cpp:89-113) in FP32 with 1e-3 m of
     // slack: the window is skipped, or the scan starts late, only where
     // every sample certainly fails the quick reject.

@@ -96,7 +96,8 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
   for (int pr = threadIdx.x; pr < m * nt; pr += blockDim.x) {
     const int e = pr / nt, j = pr % nt;
     const ViewCtx V =
-        make_view_ctx(sm.q_rx[e], sm.q_ry[e], F, radius, P.r_lt2, P.mb_le2, hts, sm.n_half);
+        make_view_ctx(sm.q_rx[e], sm.q_ry[e], F, radius, P.r_lt2, P.mb_le2, hts, sm.n_half,
+                      P.exact_only != 0);
     if ((V.gx - V.px).v < 1e-9) continue;  // behind the goal line: zero view
     PP_D1_T0();
     const PairInfo pi = pair_info(V, F.px[kTheirs + j], F.py[kTheirs + j]);
@@ -142,7 +143,8 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
     const int e = sm.iv_e[slot];
     if (sm.ch_zero[e] || sm.ch_over[e]) continue;
     const ViewCtx V =
-        make_view_ctx(sm.q_rx[e], sm.q_ry[e], F, radius, P.r_lt2, P.mb_le2, hts, sm.n_half);
+        make_view_ctx(sm.q_rx[e], sm.q_ry[e], F, radius, P.r_lt2, P.mb_le2, hts, sm.n_half,
+                      P.exact_only != 0);
     const int j = sm.iv_j[slot];
     const xd y = interval_edge_split(V, F.px[kTheirs + j], F.py[kTheirs + j], edge, sm.iv_first[slot],
                                sm.iv_last[slot], sm.iv_fast[slot], sm.iv_y1[slot], sm.iv_y2[slot],
@@ -193,7 +195,8 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
     const int e = threadIdx.x;
     View v{0.0, 0.0, 0.0, 0.0};
     if (sm.ch_over[e]) {
-      v = goal_view_thread(sm.q_rx[e], sm.q_ry[e], F, radius, P.r_lt2, P.mb_le2);
+      v = goal_view_thread(sm.q_rx[e], sm.q_ry[e], F, radius, P.r_lt2, P.mb_le2,
+                           P.exact_only != 0);
     } else if (!sm.ch_zero[e] && !((xd(0.5) * xd(F.L) - xd(sm.q_rx[e])).v < 1e-9)) {
       const xd gh = xd(0.5) * xd(F.gw);
       xd best_lo = 0.0, best_hi = 0.0, best_w = -1.0;

@@ -1,0 +1,110 @@
+"""GPU parity at BASELINE's full sizes, against the compiled reference run
+live on the host (oracle/_ref):
+
+* C3 -- frame F8 on the 1 cm grid, 1200 directions x 900 powers, flat
+  (1,080,000 cells, 17.28 M pass evaluations): the whole result block,
+  ids / times / receive points / feasibility bit-exact, every score within
+  1e-4, best_pass x3; and the same block with the FP32 shortcuts off.
+* C4 -- the running-point map at grid_step 0.01 m over all four zones
+  (543,004 vertices, offball.cpp:69-87,176-213): the vertex set and the
+  scorable flags identical, scores and features within 1e-4,
+  best_running_points identical."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from oracle import bindings as B
+from paper_1909_07717_b200 import abi
+from tests.helpers import (SCORE_RTOL, case_inputs, compare_best, compare_grid, score_close)
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not B.ref_available(), reason="oracle/_ref not built")]
+
+
+def _pinned_block(lib, n_cells):
+    nbytes = int(lib.pp_grid_bytes(n_cells))
+    ptr = lib.pp_host_alloc(nbytes)
+    assert ptr
+    return abi.GridBlock(n_cells, buf=(C.c_uint8 * nbytes).from_address(ptr)), ptr
+
+
+@pytest.mark.timeout(1200)
+def test_c3_full_grid_bit_exact(ctx, grids_golden):
+    lib = abi.load_library()
+    world, params, _, kicker, _ = case_inputs(grids_golden, "f8")
+    grid = abi.SearchGrid(1200, 900, 1.0, 6.5, 1, 0)
+    n = 1200 * 900
+    blk, ptr = _pinned_block(lib, n)
+    try:
+        assert lib.pp_dpps(ctx, C.byref(world), C.byref(params), C.byref(grid), kicker,
+                           abi.PP_COPY_ALL, ptr) == 0, lib.pp_last_error(ctx)
+        fast = bytes(blk.buf)
+        # the same frame with every FP32 shortcut off: byte-identical block
+        assert lib.pp_ctx_set_option(ctx, abi.PP_OPT_EXACT_ONLY, 1) == 0
+        try:
+            assert lib.pp_dpps(ctx, C.byref(world), C.byref(params), C.byref(grid), kicker,
+                               abi.PP_COPY_ALL, ptr) == 0, lib.pp_last_error(ctx)
+        finally:
+            lib.pp_ctx_set_option(ctx, abi.PP_OPT_EXACT_ONLY, 0)
+        blk.summary.device_ms = 0.0
+        exact = bytes(blk.buf)
+        fast = bytearray(fast)
+        off = abi.DppsSummary.device_ms.offset
+        fast[off:off + 8] = bytes(8)
+        assert bytes(fast) == exact, "C3: FP32 shortcuts changed the block"
+
+        ref = abi.GridBlock(n)
+        m = B.msgbuf()
+        assert B.ref().ref_dpps(C.byref(world), C.byref(params), C.byref(grid), kicker,
+                                os.cpu_count() or 1, ref.ptr(), m, 512) == 0, m.value
+        ours, theirs = ref.ids()
+        want = {"our_id": ours, "opp_id": theirs, "our_time": ref.our_time,
+                "opp_time": ref.opp_time, "rx": ref.rx, "ry": ref.ry, "score": ref.score,
+                "feasible": ref.feasible}
+        errs = compare_grid(blk, want, "C3") + compare_best(blk.summary, ref.summary, blk.score,
+                                                            "C3")
+        assert not errs, "\n".join(errs)
+        assert int(blk.summary.n_feasible[0]) == 566477  # SURVEY 8(c) golden count
+        assert int(blk.summary.best_cell[0]) == ref.summary.best_cell[0]
+        assert blk.summary.sbip_calls == n * 16
+    finally:
+        lib.pp_host_free(ptr)
+
+
+@pytest.mark.timeout(900)
+def test_c4_runmap_1cm(ctx, grids_golden):
+    lib = abi.load_library()
+    world, params, _, _, _ = case_inputs(grids_golden, "f8")
+    params.thresholds.grid_step = 0.01
+    nv = C.c_int64()
+    assert lib.pp_runmap_count(C.byref(world), C.byref(params), 0xF, C.byref(nv)) == 0
+    assert nv.value == 543004
+    assert B.ref().ref_runmap_count(C.byref(world), C.byref(params), 0xF) == nv.value
+    # best_running_points with the frame's best pass point excluded (CLI plan flow)
+    req = abi.RunmapRequest(0xF, 0, 4, 1, 1.2467, 1.4764, 1)
+    got = abi.RunmapBlock(nv.value)
+    assert lib.pp_runmap(ctx, C.byref(world), C.byref(params), C.byref(req), got.ptr(),
+                         nv.value) == 0, lib.pp_last_error(ctx)
+    want = abi.RunmapBlock(nv.value)
+    m = B.msgbuf()
+    assert B.ref().ref_runmap(C.byref(world), C.byref(params), C.byref(req), want.ptr(),
+                              nv.value, m, 512) == 0, m.value
+    for arr in ("px", "py", "scorable"):
+        assert np.array_equal(getattr(got, arr), getattr(want, arr)), arr
+    assert got.summary.n_scorable == want.summary.n_scorable
+    ok = want.scorable.astype(bool)
+    assert ok.sum() > 400000
+    assert np.all(score_close(got.score[ok], want.score[ok], SCORE_RTOL))
+    assert np.all(score_close(got.features[ok], want.features[ok], SCORE_RTOL))
+    assert np.all(np.isnan(got.score[~ok]))
+    gs, ws = got.summary, want.summary
+    assert gs.n_best == ws.n_best
+    assert list(gs.best_order[:gs.n_best]) == list(ws.best_order[:ws.n_best])
+    for z in range(4):
+        a, b = gs.best[z], ws.best[z]
+        assert bool(a.valid) == bool(b.valid), z
+        if a.valid:
+            assert (a.px, a.py) == (b.px, b.py) or score_close(a.score, b.score), z
+            assert score_close(a.score, b.score), z
