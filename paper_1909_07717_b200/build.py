@@ -47,6 +47,7 @@ def build_product(force: bool = False, verbose_ptxas: bool = False, profile: boo
             if f.endswith((".cu", ".cuh", ".h", ".hpp"))]
     hdrs = [os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))
             if f.endswith(".h")]
+    hdrs.append(os.path.join(ROOT, "include", "passplan", "detail", "pp_math.hpp"))
     if force or _stale(target, srcs + hdrs):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17",
                "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-shared",

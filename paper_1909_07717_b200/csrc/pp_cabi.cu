@@ -508,7 +508,7 @@ int32_t possession_of(const pp_world& w, int32_t kicker_id, const pp_params& p) 
 
 // World-independent tables of a (params, grid): unit directions and the
 // per-(kick slot, power) trajectory rows.  Built on the host with the same
-// FP64 operations as the kernels (pp_math.cuh is host/device) and uploaded
+// FP64 operations as the kernels (passplan/detail/pp_math.hpp is host/device) and uploaded
 // only when the inputs change.  Fills P.dirs / P.pows.
 cudaError_t ensure_tables(pp_ctx* ctx, pp::DevParams* P) {
   using pp::xd;

@@ -5,7 +5,9 @@
 #include <cstdint>
 
 #include "passplan_b200.h"
-#include "pp_math.cuh"
+#include <math_constants.h>
+
+#include "passplan/detail/pp_math.hpp"
 
 namespace pp {
 

@@ -14,43 +14,7 @@ namespace pp {
 // samples per robot), the first sample not rejected by the FP32 filters gets
 // the exact FP64 test, and the rest rule applies when none hits
 // (intercept.cpp:121-150).
-struct BallPath {  // BallTrajectory (ball_model.hpp:27-66) in FP64
-  Traj tr;
-  double ox, oy, ux, uy;  // origin, unit direction
-  double slide, roll;     // the trajectory's own decelerations
-};
-
-// BallTrajectory resolve (ball_model.cpp:12-43): slide_phase false = free_roll.
-__host__ __device__ inline BallPath make_path(xd ox, xd oy, xd dx, xd dy, xd speed, bool chip,
-                                              bool slide_phase, xd slide, xd roll, xd ratio,
-                                              xd chip_frac) {
-  BallPath b;
-  b.ox = ox.v;
-  b.oy = oy.v;
-  b.slide = slide.v;
-  b.roll = roll.v;
-  const xd n = xsqrt(dx * dx + dy * dy);
-  if (n.v == 0.0) {
-    b.ux = 1.0;
-    b.uy = 0.0;
-  } else {
-    b.ux = (dx / n).v;
-    b.uy = (dy / n).v;
-  }
-  Traj& t = b.tr;
-  t.speed = speed;
-  t.v1 = slide_phase ? ratio * speed : speed;
-  t.t_se = 0.0;
-  t.d_se = 0.0;
-  if (slide_phase) {
-    t.t_se = (speed - t.v1) / slide;
-    t.d_se = (speed * speed - t.v1 * t.v1) / (xd(2.0) * slide);
-  }
-  t.t_stop = t.t_se + t.v1 / roll;
-  t.d_stop = t.d_se + (t.v1 * t.v1) / (xd(2.0) * roll);
-  t.from = chip ? chip_frac * t.d_stop : xd(0.0);
-  return b;
-}
+// BallPath / make_path: passplan/detail/pp_math.hpp (shared with the host).
 
 // scan_window (intercept.cpp:47-69) of a path sampled at dt.
 __device__ __forceinline__ void path_window(const BallPath& B, const FrameDev& F, xd dt,

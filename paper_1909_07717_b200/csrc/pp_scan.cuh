@@ -17,7 +17,13 @@ namespace pp {
 // single frame's latency (one robot per warp); 4 warps x 8 CTAs/SM maximises
 // throughput when there are many tiles (batches, 1 cm grids).
 constexpr int kScanWarpsWide = 16, kScanCtasWide = 2;
-constexpr int kScanWarpsNarrow = 4, kScanCtasNarrow = 8;
+#ifndef PP_SCAN_WARPS_NARROW
+#define PP_SCAN_WARPS_NARROW 4
+#endif
+#ifndef PP_SCAN_CTAS_NARROW
+#define PP_SCAN_CTAS_NARROW 8
+#endif
+constexpr int kScanWarpsNarrow = PP_SCAN_WARPS_NARROW, kScanCtasNarrow = PP_SCAN_CTAS_NARROW;
 constexpr int kScanWarpsMid = 8, kScanCtasMid = 4;  // one wave of up to 4 x 148 tiles
 #ifndef PP_VALUE_CHUNK
 #define PP_VALUE_CHUNK 32
@@ -320,7 +326,7 @@ __device__ __forceinline__ void load_frame(FrameDev* dst_, const FrameDev* src_)
 // 12-43, intercept.cpp:12-25, 47-69; dpps.cpp:119-138).  Lane = power.
 
 
-// ray_exit_distance / travel_time_to_distance (pp_math.cuh) with xdiv.
+// ray_exit_distance / travel_time_to_distance (passplan/detail/pp_math.hpp) with xdiv.
 __device__ __forceinline__ xd ray_exit_distance_d(xd L, xd W, xd ox, xd oy, xd ux, xd uy) {
   const xd hx = xd(0.5) * L;
   const xd hy = xd(0.5) * W;
@@ -527,6 +533,35 @@ __device__ __forceinline__ void pair_result(const CellLane& c, const DevParams& 
   *code_out = code;
 }
 
+// First sample worth testing for robot ri on cell c (ke when none):
+// scan_robot's prunes (intercept.cpp:89-113) in FP32 with 1e-3 m of slack --
+// the window is skipped, or the scan starts late, only where every sample
+// certainly fails the quick reject.  Exact-only mode: the window start.
+__device__ __forceinline__ int scan_start(const CellLane& c, const SampleF& S, const FrameDev& F,
+                                          int ri) {
+  const int kb = c.kb;
+  const int ke = c.valid ? c.ke : 0;
+  if (!(c.valid && kb < ke)) return ke;
+  if (S.exact) return kb;
+  const int slot = F.scan_slot[ri];
+  const float rx0 = static_cast<float>(F.px[slot]), ry0 = static_cast<float>(F.py[slot]);
+  const float ax = static_cast<float>(c.ax), ay = static_cast<float>(c.ay);
+  const float abx = static_cast<float>(c.bx) - ax;
+  const float aby = static_cast<float>(c.by) - ay;
+  const float len2 = abx * abx + aby * aby;
+  float tt = len2 > 0.f ? __fdividef((rx0 - ax) * abx + (ry0 - ay) * aby, len2) : 0.f;
+  tt = fminf(fmaxf(tt, 0.f), 1.f);
+  const float ex = ax + abx * tt - rx0, ey = ay + aby * tt - ry0;
+  const float gap = sqrt_a(ex * ex + ey * ey) - 1e-3f - S.radf;
+  if (gap > S.vbf * static_cast<float>(ke - 1) * S.dtf * 1.0001f) return ke;
+  int k = kb;
+  if (S.vbf > 0.f && gap > 0.f) {
+    const int kk = static_cast<int>(floorf(gap / (S.vbf * S.dtf * 1.0001f))) - 1;
+    k = kk > kb ? (kk < ke ? kk : ke) : kb;
+  }
+  return k;
+}
+
 // B of the scan for robot `ri` (one warp, lane = cell): scan_robot
 // (intercept.cpp:87-115) + first feasible sample (kernel.hpp:33-44) + rest
 // rule (dpps.cpp:177-190).  Two exact-safe accelerations, neither of which
@@ -547,34 +582,8 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
                                            int ri, int max_steps, double* t_out,
                                            int* code_out, int* left_k) {
   const int lane = threadIdx.x & 31;
-  const bool valid = c.valid;
-  const int kb = c.kb;
-  const int ke = valid ? c.ke : 0;
-  int k = ke;
-  if (valid && kb < ke && S.exact) {
-    k = kb;  // no FP32 prunes: every in-window sample is tested
-  } else if (valid && kb < ke) {
-    // scan_robot's prunes (intercept.cpp:89-113) in FP32 with 1e-3 m of
-    // slack: the window is skipped, or the scan starts late, only where
-    // every sample certainly fails the quick reject.
-    const int slot = F.scan_slot[ri];
-    const float rx0 = static_cast<float>(F.px[slot]), ry0 = static_cast<float>(F.py[slot]);
-    const float ax = static_cast<float>(c.ax), ay = static_cast<float>(c.ay);
-    const float abx = static_cast<float>(c.bx) - ax;
-    const float aby = static_cast<float>(c.by) - ay;
-    const float len2 = abx * abx + aby * aby;
-    float tt = len2 > 0.f ? __fdividef((rx0 - ax) * abx + (ry0 - ay) * aby, len2) : 0.f;
-    tt = fminf(fmaxf(tt, 0.f), 1.f);
-    const float ex = ax + abx * tt - rx0, ey = ay + aby * tt - ry0;
-    const float gap = sqrt_a(ex * ex + ey * ey) - 1e-3f - S.radf;
-    if (!(gap > S.vbf * static_cast<float>(ke - 1) * S.dtf * 1.0001f)) {
-      k = kb;
-      if (S.vbf > 0.f && gap > 0.f) {
-        const int kk = static_cast<int>(floorf(gap / (S.vbf * S.dtf * 1.0001f))) - 1;
-        k = kk > kb ? (kk < ke ? kk : ke) : kb;
-      }
-    }
-  }
+  const int ke = c.valid ? c.ke : 0;
+  int k = scan_start(c, S, F, ri);
   const TrajF trf = trf_in;
   int hit = -1;
   bool capped = false;
@@ -928,7 +937,42 @@ __device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, cons
     //        could possibly get there, d <= radius + D(t) (ReachBound).
     const CellLane* cl = reinterpret_cast<const CellLane*>(sm.cl_raw);
     const int max_steps = kLeftovers ? P.scan_steps : 1 << 30;
-    for (int ri = warp; ri < F.n_scan; ri += nwarps) {
+    // Robot order (throughput shape): the robots nearest the tile's ray
+    // first -- the longest scans, and the earliest team caps -- pulled
+    // dynamically by the warps (sm.next_pair counts robots here), so the
+    // warps reach the barrier together.  Every warp ranks the robots the
+    // same way (lane = robot); order does not change results.
+#ifndef PP_SCAN_STATIC_ORDER
+    constexpr bool kDyn = !kLeftovers;
+#else
+    constexpr bool kDyn = false;  // dev knob: round-robin robots (round-1 order)
+#endif
+    int my_rank = 0;
+    if (kDyn) {
+      float key = 3.0e38f;
+      if (lane < F.n_scan) {
+        const RobotK& rk = sm.rk[lane];
+        const float2 u = sm.tile_uf;
+        const float along = fmaxf(-(rk.bxf * u.x + rk.byf * u.y), 0.f);  // robot - ball on u
+        const float ex = -rk.bxf - along * u.x, ey = -rk.byf - along * u.y;
+        key = ex * ex + ey * ey;
+      }
+      for (int j = 0; j < 32; ++j) {
+        const float kj = __shfl_sync(0xffffffffu, key, j);
+        my_rank += (kj < key || (kj == key && j < lane)) ? 1 : 0;
+      }
+    }
+    for (int it = warp;; it = kDyn ? it : it + nwarps) {
+      int ri = it;
+      if (kDyn) {
+        unsigned i = 0;
+        if (lane == 0) i = atomicAdd(&sm.next_pair, 1u);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i >= static_cast<unsigned>(F.n_scan)) break;
+        ri = __ffs(__ballot_sync(0xffffffffu, my_rank == static_cast<int>(i))) - 1;
+      } else if (ri >= F.n_scan) {
+        break;
+      }
       const RobotK& rk = sm.rk[ri];
       const SampleF S = sample_f(rk, sm.tile_uf, P);
       double time;
