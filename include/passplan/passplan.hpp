@@ -2,16 +2,21 @@
 //
 // Source-compatible with the declarations a caller of the reference uses on
 // this path (reference headers proj/include/passplan/{vec2,world,errors,
-// weights,ball_model,motion,dpps,pass_eval,offball,config}.hpp): same
-// namespace, type and field names, defaults, signatures and error categories.
-// The per-header names (passplan/dpps.hpp, ...) are provided as one-line
-// forwarders to this file.  Every computation on the hot path runs on the
-// GPU through the C-ABI of passplan_b200.h; the small host-side helpers here
-// (geometry, tables, lattices, validation) are the same closed forms.
+// weights,ball_model,motion,dpps,pass_eval,offball,intercept,config,csv,
+// snapshot}.hpp and detail/arrival_math.hpp): same namespace, type and field
+// names, defaults, signatures and error categories.  The per-header names
+// (passplan/dpps.hpp, ...) are provided as one-line forwarders to this file;
+// detail/arrival_math.hpp forwards to the shared restatement pp_math.hpp.
+// Every computation on the hot path runs on the GPU through the C-ABI of
+// passplan_b200.h; the small host-side helpers here (geometry, tables,
+// lattices, validation, the closed-form ball model) are the same closed forms.
 //
-// Not provided (outside the accelerated path): JSON snapshot/config I/O,
-// CSV/SVG emitters, CLI, decide_shot / plan_free_kick / possession,
-// drag_decision, SvgStyle.
+// Not provided (outside the accelerated path, SURVEY.md 2 out of scope): the
+// SVG renderer (svg.hpp, SvgStyle), drag_decision / DragDecision, and the
+// per-pair plug-in point kernels::KernelBackend with detail_intercept's
+// scan_window / make_kin / scan_robot (one call there is a single
+// (trajectory, robot) pair; the GPU replaces the layer above, run_dpps --
+// telemetry.kernel names the backend "sm100a").
 #pragma once
 
 #include <array>
@@ -362,6 +367,14 @@ struct RunningPoint {
   RunningPointFeatures features;
 };
 
+// guard_time (offball.hpp:72): the two opponents nearest their defense area
+// race to the guard points; capped at `cap`.  guard_points (offball.hpp:75):
+// where the segments from p to the two posts enter the defense area.  Both
+// throw domain_error for p strictly inside the area (and guard_time for a
+// cap that is not positive and finite).  Computed on the GPU.
+double guard_time(Vec2 p, const WorldState& world, const MotionLimits& limits, double cap = 10.0);
+std::pair<Vec2, Vec2> guard_points(const FieldGeometry& field, Vec2 p);
+
 std::vector<Vec2> zone_lattice(const Zone& zone, double step);
 std::vector<RunningPoint> best_running_points(const WorldState& world,
                                               const std::set<ZoneLabel>& occupied,
@@ -371,12 +384,16 @@ std::vector<RunningPoint> best_running_points(const WorldState& world,
 // ---- ball trajectory (ball_model.hpp) ------------------------------------------
 struct BallTrajectory {
   Vec2 origin;
-  Vec2 direction;  // unit
+  Vec2 direction;  // unit; arbitrary when kick_speed == 0
   double kick_speed = 0.0;
   KickType kick_type = KickType::flat;
-  double slide_decel = 0.0, roll_decel = 0.0;
-  double v1 = 0.0, slide_end_time = 0.0, slide_end_distance = 0.0;
-  double stop_time = 0.0, stop_distance = 0.0;
+  double v1 = 0.0;  // speed at the slide-to-roll transition
+  double slide_decel = 0.0;
+  double roll_decel = 0.0;
+  double slide_end_time = 0.0;
+  double slide_end_distance = 0.0;
+  double stop_time = 0.0;
+  double stop_distance = 0.0;
   double interceptable_from = 0.0;  // chip: airborne until this distance
 
   static BallTrajectory flat_kick(Vec2 origin, Vec2 dir, double speed,
@@ -391,6 +408,17 @@ struct BallTrajectory {
   std::optional<double> travel_time_to_distance(double d) const;
   std::optional<double> time_of_first_interceptable_point(double d) const;
 };
+
+struct BallSample {
+  Vec2 position;
+  double speed = 0.0;
+  bool airborne = false;
+};
+
+// Checked free forms (ball_model.hpp:68-81): domain_error on t < 0 / d < 0 / NaN.
+BallSample ball_state_at(const BallTrajectory& traj, double t);
+std::optional<double> travel_time_to_distance(const BallTrajectory& traj, double d);
+std::optional<double> time_of_first_interceptable_point(const BallTrajectory& traj, double d);
 
 struct PassPower {
   double kick_speed = 0.0;
@@ -415,6 +443,23 @@ std::vector<InterceptResult> intercept_all(const WorldState& world, const BallTr
                                            const MotionLimits& theirs_limits, double dt,
                                            double robot_radius = 0.09);
 double arrival_time(const RobotState& robot, Vec2 target, const MotionLimits& limits);
+// arrival_time + buffer (motion.hpp:25); domain_error on a negative or NaN buffer.
+double arrival_time_with_buffer(const RobotState& robot, Vec2 target, const MotionLimits& limits,
+                                double buffer);
+
+// Sampled trajectory (intercept.hpp:25-33): ts[k] = k*dt, ss[k] = distance_at(ts[k]),
+// k = 0 .. floor(stop_time/dt + 1e-9).  domain_error unless dt > 0.
+struct TrajectorySamples {
+  std::vector<double> ts;
+  std::vector<double> ss;
+  double dt = 0.0;
+  int count() const { return static_cast<int>(ts.size()); }
+  static TrajectorySamples build(const BallTrajectory& traj, double dt);
+};
+
+// Distance along unit u from origin to the field boundary (intercept.hpp:35-37);
+// nullopt when the origin is outside the field.
+std::optional<double> ray_exit_distance(const FieldGeometry& field, Vec2 origin, Vec2 u);
 
 // ---- shot, free kick, possession (pass_eval.hpp) --------------------------------
 enum class ShotReason { angle_too_small, interceptable, clear };

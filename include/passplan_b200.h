@@ -296,6 +296,17 @@ pp_status pp_score_running_points(pp_ctx* ctx, const pp_world* world, const pp_p
                                   double* score_out, pp_run_features* features_out,
                                   uint8_t* ok_out);
 
+/* guard_points (offball.hpp:75, offball.cpp:125-135) and guard_time
+ * (offball.hpp:72, offball.cpp:137-174) at n points of the plane.  The
+ * guards are the world's opponents ranked by distance to their defense area
+ * (ties by id); `limits` are the guards' motion limits.  cap must be positive
+ * and finite (PP_DOMAIN otherwise, as guard_time throws).  guard_pq: n x 4
+ * doubles (P.x, P.y, Q.x, Q.y) or NULL; guard_time: n or NULL; ok[i] = 0
+ * where the reference throws domain_error (strictly inside the area). */
+pp_status pp_guard_points(pp_ctx* ctx, const pp_world* world, const pp_motion_limits* limits,
+                          double cap, int64_t n, const double* px, const double* py,
+                          double* guard_pq, double* guard_time, uint8_t* ok_out);
+
 /* ---- batched frames (log replay / what-if states) ----------------------
  * Independent frames share params and grid; each gets the pp_dpps summary.
  * kicker_ids may be NULL: then the kicker is the teammate nearest the ball

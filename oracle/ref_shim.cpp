@@ -649,6 +649,33 @@ int ref_plan_free_kick(const pp_world* world, const pp_params* params, int32_t k
   });
 }
 
+// guard_points + guard_time of the reference at n points (offball.cpp:125-174);
+// ok[i] = 0 where either throws (point strictly inside the area).
+int ref_guard_points(const pp_world* world, const pp_motion_limits* limits, double cap, int64_t n,
+                     const double* px, const double* py, double* pq, double* t, uint8_t* ok,
+                     char* msg, size_t msg_len) {
+  return guarded(msg, msg_len, [&] {
+    const WorldState w = to_world(*world);
+    MotionLimits lim;
+    lim.max_speed = limits->max_speed;
+    lim.max_accel = limits->max_accel;
+    lim.max_decel = limits->max_decel;
+    for (int64_t i = 0; i < n; ++i) {
+      try {
+        const auto g = guard_points(w.field, {px[i], py[i]});
+        pq[4 * i] = g.first.x;
+        pq[4 * i + 1] = g.first.y;
+        pq[4 * i + 2] = g.second.x;
+        pq[4 * i + 3] = g.second.y;
+        t[i] = guard_time({px[i], py[i]}, w, lim, cap);
+        ok[i] = 1;
+      } catch (const Error&) {
+        ok[i] = 0;
+      }
+    }
+  });
+}
+
 // `passplan plan --out` CSV of one frame (passplan_main.cpp:89, csv.cpp:85-114).
 // Returns the text length (buf gets a NUL-terminated copy, truncated to len).
 int64_t ref_grid_csv(const pp_world* world, const pp_params* params, int32_t kicker_id,

@@ -302,6 +302,9 @@ def _declare(lib):
     lib.pp_score_running_points.argtypes = [vp, _P(World), _P(Params), C.c_int64, dp, dp, dp,
                                             _P(RunFeatures), _P(C.c_uint8)]
     lib.pp_score_running_points.restype = C.c_int
+    lib.pp_guard_points.argtypes = [vp, _P(World), _P(MotionLimits), C.c_double, C.c_int64, dp,
+                                    dp, dp, dp, _P(C.c_uint8)]
+    lib.pp_guard_points.restype = C.c_int
     lib.pp_dpps_batch.argtypes = [vp, _P(World), C.c_int64, _P(Params), _P(SearchGrid),
                                   _P(C.c_int32), _P(DppsSummary)]
     lib.pp_batch_upload.argtypes = [vp, _P(World), C.c_int64, _P(C.c_int32)]
@@ -355,5 +358,5 @@ EXPORTED_SYMBOLS = (
     "pp_dpps_batch", "pp_batch_upload", "pp_batch_run", "pp_batch_download", "pp_dpps_frames",
     "pp_batch_kernel_times",
     "pp_score_running_points", "pp_kick_trajectory", "pp_intercept_all", "pp_possession",
-    "pp_decide_shot", "pp_plan_free_kick",
+    "pp_decide_shot", "pp_plan_free_kick", "pp_guard_points",
 )

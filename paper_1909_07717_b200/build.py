@@ -115,6 +115,34 @@ def build_cpp_tests(force: bool = False) -> str:
     return CPP_TEST
 
 
+REF_ACCEPTANCE = os.path.join(ROOT, "tests", "cpp", "build", "ref_acceptance")
+REF_TESTS = "/root/reference/proj/tests"
+
+
+def build_ref_acceptance(force: bool = False):
+    """tests/cpp/build/ref_acceptance: the reference's own acceptance gate
+    (proj/tests/acceptance_main.cpp + oracles.hpp, compiled where they lie,
+    unmodified) linked against the drop-in (include/passplan +
+    lib/libpassplan.so) instead of the reference library.  The only addition
+    is the test-only drag_decision stub tests/cpp/acceptance_stub.hpp
+    (out-of-scope drag skill).  Built when the reference tree exists (this
+    container); the binary travels to the GPU box, which has no reference."""
+    src = os.path.join(REF_TESTS, "acceptance_main.cpp")
+    if not os.path.exists(src):
+        return None
+    stub = os.path.join(ROOT, "tests", "cpp", "acceptance_stub.hpp")
+    hdrs = [os.path.join(ROOT, "include", "passplan", f)
+            for f in os.listdir(os.path.join(ROOT, "include", "passplan")) if f.endswith(".hpp")]
+    os.makedirs(os.path.dirname(REF_ACCEPTANCE), exist_ok=True)
+    if force or _stale(REF_ACCEPTANCE, [src, stub, DROPIN_LIB] + hdrs):
+        data = os.path.join(ROOT, "tests", "golden", "data")
+        _run([shutil.which("g++") or "g++", "-std=c++20", "-O2", "-ffp-contract=off",
+              "-I", os.path.join(ROOT, "include"), "-I", REF_TESTS, "-include", stub,
+              f'-DPASSPLAN_DATA_DIR="{data}"', src, "-o", REF_ACCEPTANCE,
+              "-L", LIB_DIR, "-lpassplan", "-lpassplan_b200", f"-Wl,-rpath,{LIB_DIR}"])
+    return REF_ACCEPTANCE
+
+
 def build_checkers() -> None:
     """oracle/liboracle.so always; oracle/_ref/ when the reference tree exists
     (this container).  The GPU box only uses the prebuilt files."""
@@ -131,6 +159,7 @@ def build_all(force: bool = False) -> None:
     build_cli(force=force)
     build_checkers()
     build_cpp_tests(force=force)
+    build_ref_acceptance(force=force)
 
 
 if __name__ == "__main__":

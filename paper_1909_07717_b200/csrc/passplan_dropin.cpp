@@ -12,6 +12,7 @@
 #include <cstring>
 #include <string>
 
+#include "passplan/detail/pp_math.hpp"
 #include "passplan/passplan.hpp"
 #include "passplan_b200.h"
 
@@ -23,10 +24,29 @@ namespace {
 // re-entrant; a pp_ctx is single-threaded).
 struct ThreadCtx {
   pp_ctx* ctx = nullptr;
-  void* block = nullptr;
+  void* block = nullptr;  // scratch result block (run maps)
   size_t block_bytes = 0;
+  // The last run_dpps of this thread: its result block (summary with the
+  // fused best_pass for all / flat / chip, per-cell outputs) and the inputs
+  // it was computed from.  best_pass on a grid that still matches it is
+  // served from the summary without re-scoring (run_dpps then
+  // best_pass x3 is the reference's own plan sequence).
+  void* dpps_block = nullptr;
+  size_t dpps_bytes = 0;
+  bool dpps_valid = false;
+  int64_t dpps_cells = 0;
+  pp_world dpps_world;
+  pp_params dpps_params;
+  pp_search_grid dpps_grid;
+  // direction_table / power_table of the last grid shape
+  int dir_n = -1;
+  std::vector<Vec2> dirs;
+  int pow_n = -1;
+  double pow_lo = 0.0, pow_hi = 0.0;
+  std::vector<double> pows;
   ~ThreadCtx() {
     if (block) pp_host_free(block);
+    if (dpps_block) pp_host_free(dpps_block);
     if (ctx) pp_ctx_destroy(ctx);
   }
 };
@@ -46,15 +66,20 @@ pp_ctx* context() {
   return tl.ctx;
 }
 
-void* host_block(size_t bytes) {
-  if (bytes > tl.block_bytes) {
-    if (tl.block) pp_host_free(tl.block);
-    tl.block = pp_host_alloc(bytes);
-    if (!tl.block) throw internal_error("passplan: pinned host allocation failed");
-    tl.block_bytes = bytes;
+void* grow_pinned(void** p, size_t* have, size_t bytes) {
+  if (bytes > *have) {
+    if (*p) pp_host_free(*p);
+    *p = pp_host_alloc(bytes);
+    if (!*p) {
+      *have = 0;
+      throw internal_error("passplan: pinned host allocation failed");
+    }
+    *have = bytes;
   }
-  return tl.block;
+  return *p;
 }
+
+void* host_block(size_t bytes) { return grow_pinned(&tl.block, &tl.block_bytes, bytes); }
 
 ErrorCategory category_of(pp_status st) {
   switch (st) {
@@ -327,10 +352,16 @@ CandidateGrid run_dpps(const WorldState& world, int kicker_id, const SearchGrid&
   const pp_params p = to_pp(cfg);
   const pp_search_grid g = to_pp(grid);
   const int64_t n = pp_grid_cells(&g);
-  void* block = host_block(pp_grid_bytes(n));
+  tl.dpps_valid = false;
+  void* block = grow_pinned(&tl.dpps_block, &tl.dpps_bytes, pp_grid_bytes(n));
   const auto t0 = std::chrono::steady_clock::now();
   check(pp_dpps(ctx, &w, &p, &g, kicker_id, PP_COPY_ALL, block), ctx);
   const auto t1 = std::chrono::steady_clock::now();
+  tl.dpps_valid = true;
+  tl.dpps_cells = n;
+  tl.dpps_world = w;
+  tl.dpps_params = p;
+  tl.dpps_grid = g;
   pp_grid_view v;
   pp_grid_view_of(block, n, &v);
   const pp_dpps_summary& s = *v.summary;
@@ -340,8 +371,18 @@ CandidateGrid run_dpps(const WorldState& world, int kicker_id, const SearchGrid&
   out.kicker_id = kicker_id;
   out.ball_origin = world.ball.position;
   out.kick_types = grid.kick_types();
-  out.directions = direction_table(grid.n_directions);
-  out.powers = power_table(grid.n_powers, grid.power_min, grid.power_max);
+  if (tl.dir_n != grid.n_directions) {
+    tl.dirs = direction_table(grid.n_directions);
+    tl.dir_n = grid.n_directions;
+  }
+  out.directions = tl.dirs;
+  if (tl.pow_n != grid.n_powers || tl.pow_lo != grid.power_min || tl.pow_hi != grid.power_max) {
+    tl.pows = power_table(grid.n_powers, grid.power_min, grid.power_max);
+    tl.pow_n = grid.n_powers;
+    tl.pow_lo = grid.power_min;
+    tl.pow_hi = grid.power_max;
+  }
+  out.powers = tl.pows;
   out.cells.resize(static_cast<size_t>(n));
   const int nd = grid.n_directions, np = grid.n_powers;
   for (int64_t i = 0; i < n; ++i) {
@@ -401,8 +442,54 @@ std::pair<double, PassFeatures> score_pass(const PassCandidate& candidate, const
   return {score, from_pp(f)};
 }
 
+namespace {
+
+// best_pass served from this thread's last run_dpps summary when `g` is still
+// that run's grid (same shape, every cell's feasibility and, for feasible
+// cells, the receive point and both times as computed) and world/cfg are the
+// inputs it ran on; false otherwise.  One pass over the cells, no GPU work.
+bool cached_best_pass(const CandidateGrid& g, const WorldState& world, const PlannerConfig& cfg,
+                      std::optional<KickType> only, std::optional<ScoredPass>* out) {
+  if (!tl.dpps_valid || static_cast<int64_t>(g.cells.size()) != tl.dpps_cells) return false;
+  const pp_search_grid gg = to_pp(g.grid);
+  if (std::memcmp(&gg, &tl.dpps_grid, sizeof(gg)) != 0) return false;
+  if (g.kick_types != g.grid.kick_types()) return false;
+  if (world.ours.size() > PP_MAX_TEAM || world.theirs.size() > PP_MAX_TEAM) return false;
+  const pp_world w = to_pp(world);
+  if (std::memcmp(&w, &tl.dpps_world, sizeof(w)) != 0) return false;
+  const pp_params p = to_pp(cfg);
+  if (std::memcmp(&p, &tl.dpps_params, sizeof(p)) != 0) return false;
+  pp_grid_view v;
+  pp_grid_view_of(tl.dpps_block, tl.dpps_cells, &v);
+  const int nd = g.grid.n_directions, np = g.grid.n_powers;
+  for (int64_t i = 0; i < tl.dpps_cells; ++i) {
+    const PassCandidate& c = g.cells[static_cast<size_t>(i)];
+    if (c.feasible != (v.feasible[i] != 0)) return false;
+    if (!c.feasible) continue;
+    if (c.kick_type != g.kick_types[static_cast<size_t>(i / (int64_t(nd) * np))] ||
+        c.dir_index != static_cast<int>((i / np) % nd) || c.power_index != static_cast<int>(i % np) ||
+        c.our_time != v.our_time[i] || c.opp_time != v.opp_time[i] ||
+        c.receive_point.x != v.rx[i] || c.receive_point.y != v.ry[i])
+      return false;
+  }
+  const pp_dpps_summary& s = *v.summary;
+  const int which = !only ? 0 : (*only == KickType::flat ? 1 : 2);
+  const int64_t b = s.best_cell[which];
+  if (b < 0) {
+    out->reset();
+  } else {
+    *out = ScoredPass{g.cells[static_cast<size_t>(b)], s.best_score[which],
+                      from_pp(s.best_features[which])};
+  }
+  return true;
+}
+
+}  // namespace
+
 std::optional<ScoredPass> best_pass(const CandidateGrid& g, const WorldState& world,
                                     const PlannerConfig& cfg, std::optional<KickType> only) {
+  std::optional<ScoredPass> cached;
+  if (cached_best_pass(g, world, cfg, only, &cached)) return cached;
   std::vector<size_t> idx;
   for (size_t i = 0; i < g.cells.size(); ++i) {
     const PassCandidate& c = g.cells[i];
@@ -501,6 +588,35 @@ std::pair<double, RunningPointFeatures> score_running_point(Vec2 pt, const World
   return {score, from_pp(feat)};
 }
 
+namespace {
+
+// guard_points_kernel on one point: {P, Q} and the guard time.
+std::pair<std::pair<Vec2, Vec2>, double> guard_query(Vec2 p, const WorldState& world,
+                                                     const MotionLimits& limits, double cap) {
+  pp_ctx* ctx = context();
+  const pp_world w = to_pp(world);
+  const pp_motion_limits lim{limits.max_speed, limits.max_accel, limits.max_decel};
+  double pq[4];
+  double t = 0.0;
+  uint8_t ok = 0;
+  check(pp_guard_points(ctx, &w, &lim, cap, 1, &p.x, &p.y, pq, &t, &ok), ctx);
+  if (!ok) throw domain_error("guard points undefined: point inside the defense area");
+  return {{{pq[0], pq[1]}, {pq[2], pq[3]}}, t};
+}
+
+}  // namespace
+
+double guard_time(Vec2 p, const WorldState& world, const MotionLimits& limits, double cap) {
+  if (!(cap > 0.0) || !std::isfinite(cap)) throw domain_error("guard time cap must be positive");
+  return guard_query(p, world, limits, cap).second;
+}
+
+std::pair<Vec2, Vec2> guard_points(const FieldGeometry& field, Vec2 p) {
+  WorldState w;  // no opponents: only the geometry is computed
+  w.field = field;
+  return guard_query(p, w, MotionLimits{}, 10.0).first;
+}
+
 std::vector<RunningPoint> best_running_points(const WorldState& world,
                                               const std::set<ZoneLabel>& occupied,
                                               const PlannerConfig& cfg, int n_runners,
@@ -566,7 +682,9 @@ std::vector<FrameBest> best_pass_batch(const std::vector<WorldState>& frames,
   return out;
 }
 
-// ---- ball trajectory (ball_model.cpp:12-146), host ------------------------------
+// ---- ball trajectory (ball_model.cpp:12-146), host -------------------------------
+// The closed forms come from the one shared restatement, pp_math.hpp (the same
+// functions the kernels use); only argument checks and type mapping live here.
 namespace {
 
 BallTrajectory resolve_trajectory(Vec2 origin, Vec2 dir, double speed, KickType type,
@@ -574,29 +692,37 @@ BallTrajectory resolve_trajectory(Vec2 origin, Vec2 dir, double speed, KickType 
   params.validate();
   if (!(speed >= 0.0) || !std::isfinite(speed))
     throw domain_error("kick speed must be finite and non-negative");
+  if (dir.norm() == 0.0 && speed > 0.0) throw domain_error("kick direction must be non-zero");
+  const pp::BallPath b =
+      pp::make_path(origin.x, origin.y, dir.x, dir.y, speed, type == KickType::chip, slide_phase,
+                    params.slide_decel, params.roll_decel, params.transition_ratio,
+                    params.chip_flight_fraction);
   BallTrajectory t;
   t.origin = origin;
+  t.direction = {b.ux, b.uy};
   t.kick_speed = speed;
   t.kick_type = type;
-  t.slide_decel = params.slide_decel;
-  t.roll_decel = params.roll_decel;
-  const double n = dir.norm();
-  if (n == 0.0) {
-    if (speed > 0.0) throw domain_error("kick direction must be non-zero");
-    t.direction = {1.0, 0.0};
-  } else {
-    t.direction = {dir.x / n, dir.y / n};
-  }
-  t.v1 = slide_phase ? params.transition_ratio * speed : speed;
-  if (slide_phase) {
-    t.slide_end_time = (speed - t.v1) / params.slide_decel;
-    t.slide_end_distance = (speed * speed - t.v1 * t.v1) / (2.0 * params.slide_decel);
-  }
-  t.stop_time = t.slide_end_time + t.v1 / params.roll_decel;
-  t.stop_distance = t.slide_end_distance + (t.v1 * t.v1) / (2.0 * params.roll_decel);
-  t.interceptable_from =
-      type == KickType::chip ? params.chip_flight_fraction * t.stop_distance : 0.0;
+  t.v1 = b.tr.v1.v;
+  t.slide_decel = b.slide;
+  t.roll_decel = b.roll;
+  t.slide_end_time = b.tr.t_se.v;
+  t.slide_end_distance = b.tr.d_se.v;
+  t.stop_time = b.tr.t_stop.v;
+  t.stop_distance = b.tr.d_stop.v;
+  t.interceptable_from = b.tr.from.v;
   return t;
+}
+
+pp::Traj profile_of(const BallTrajectory& t) {
+  pp::Traj p;
+  p.speed = t.kick_speed;
+  p.v1 = t.v1;
+  p.t_se = t.slide_end_time;
+  p.d_se = t.slide_end_distance;
+  p.t_stop = t.stop_time;
+  p.d_stop = t.stop_distance;
+  p.from = t.interceptable_from;
+  return p;
 }
 
 pp_trajectory to_pp(const BallTrajectory& t) {
@@ -630,6 +756,10 @@ InterceptResult from_pp(const pp_intercept& r) {
   return o;
 }
 
+void check_nonneg(double v, const char* what) {
+  if (std::isnan(v) || v < 0.0) throw domain_error(what);
+}
+
 }  // namespace
 
 BallTrajectory BallTrajectory::flat_kick(Vec2 origin, Vec2 dir, double speed,
@@ -648,18 +778,11 @@ BallTrajectory BallTrajectory::free_roll(Vec2 origin, Vec2 velocity,
 }
 
 double BallTrajectory::speed_at(double t) const {
-  if (t < slide_end_time) return kick_speed - slide_decel * t;
-  if (t < stop_time) return v1 - roll_decel * (t - slide_end_time);
-  return 0.0;
+  return pp::speed_at(profile_of(*this), slide_decel, roll_decel, t).v;
 }
 
 double BallTrajectory::distance_at(double t) const {
-  if (t < slide_end_time) return kick_speed * t - 0.5 * slide_decel * t * t;
-  if (t < stop_time) {
-    const double u = t - slide_end_time;
-    return slide_end_distance + v1 * u - 0.5 * roll_decel * u * u;
-  }
-  return stop_distance;
+  return pp::distance_at(profile_of(*this), slide_decel, roll_decel, t).v;
 }
 
 bool BallTrajectory::airborne_at(double t) const {
@@ -667,15 +790,9 @@ bool BallTrajectory::airborne_at(double t) const {
 }
 
 std::optional<double> BallTrajectory::travel_time_to_distance(double d) const {
-  if (d == 0.0) return 0.0;
-  if (d > stop_distance) return std::nullopt;
-  if (d <= slide_end_distance) {  // stable root of d = v0 t - a t^2 / 2
-    const double rad = kick_speed * kick_speed - 2.0 * slide_decel * d;
-    return 2.0 * d / (kick_speed + std::sqrt(rad < 0.0 ? 0.0 : rad));
-  }
-  const double rem = d - slide_end_distance;
-  const double rad = v1 * v1 - 2.0 * roll_decel * rem;
-  return slide_end_time + 2.0 * rem / (v1 + std::sqrt(rad < 0.0 ? 0.0 : rad));
+  const double t = pp::travel_time_to_distance(profile_of(*this), slide_decel, roll_decel, d).v;
+  if (std::isnan(t)) return std::nullopt;  // beyond the rollout
+  return t;
 }
 
 std::optional<double> BallTrajectory::time_of_first_interceptable_point(double d) const {
@@ -683,58 +800,64 @@ std::optional<double> BallTrajectory::time_of_first_interceptable_point(double d
   return travel_time_to_distance(d);
 }
 
+BallSample ball_state_at(const BallTrajectory& traj, double t) {
+  check_nonneg(t, "ball_state_at: t must be >= 0");
+  return {traj.position_at(t), traj.speed_at(t), traj.airborne_at(t)};
+}
+
+std::optional<double> travel_time_to_distance(const BallTrajectory& traj, double d) {
+  check_nonneg(d, "travel_time_to_distance: d must be >= 0");
+  return traj.travel_time_to_distance(d);
+}
+
+std::optional<double> time_of_first_interceptable_point(const BallTrajectory& traj, double d) {
+  check_nonneg(d, "time_of_first_interceptable_point: d must be >= 0");
+  return traj.time_of_first_interceptable_point(d);
+}
+
 PassPower pass_power_for(double d, double t, const BallModelParams& params) {
   params.validate();  // ball_model.cpp:129-146
   if (!(d > 0.0) || !std::isfinite(d)) throw domain_error("pass_power_for: d must be > 0");
   if (!(t > 0.0) || !std::isfinite(t)) throw domain_error("pass_power_for: t must be > 0");
   PassPower p;
-  p.v1 = d / t + 0.5 * params.roll_decel * t;
-  p.kick_speed = p.v1 / params.transition_ratio;
-  if (p.kick_speed < params.power_min) {
-    p.kick_speed = params.power_min;
-    p.clamped = true;
-  } else if (p.kick_speed > params.power_max) {
-    p.kick_speed = params.power_max;
-    p.clamped = true;
-  }
+  p.v1 = pp::pass_power_v1(d, t, params.roll_decel).v;
+  const double raw = p.v1 / params.transition_ratio;
+  p.kick_speed = std::clamp(raw, params.power_min, params.power_max);
+  p.clamped = p.kick_speed != raw;
   return p;
 }
 
 double arrival_time(const RobotState& robot, Vec2 target, const MotionLimits& limits) {
-  // motion.cpp:16-29 with detail/arrival_math.hpp:15-69 (radius 0)
-  const double qx = target.x - robot.position.x, qy = target.y - robot.position.y;
-  const double d2 = qx * qx + qy * qy;
-  const double a = limits.max_accel, b = limits.max_decel, vmax = limits.max_speed;
-  auto rest_to_rest = [&](double L) {
-    const double peak = std::sqrt((2.0 * a) * b * L / (a + b));
-    if (peak <= vmax) return peak / a + peak / b;
-    const double d_used = (vmax * vmax) / (2.0 * a) + (vmax * vmax) / (2.0 * b);
-    return vmax / a + vmax / b + (L - d_used) / vmax;
-  };
-  auto one_d = [&](double v0, double dist) {
-    const double brake = (v0 * v0) / (2.0 * b);
-    if (v0 < 0.0 || brake > dist) {
-      const double gap = brake - std::copysign(dist, v0);
-      return std::fabs(v0) / b + rest_to_rest(gap);
-    }
-    const double peak = std::sqrt(((2.0 * a) * b * dist + b * (v0 * v0)) / (a + b));
-    if (peak <= vmax) return (peak - v0) / a + peak / b;
-    if (v0 <= vmax) {
-      const double d_used = (vmax * vmax - v0 * v0) / (2.0 * a) + (vmax * vmax) / (2.0 * b);
-      return (vmax - v0) / a + vmax / b + (dist - d_used) / vmax;
-    }
-    const double d_used = (v0 * v0 - vmax * vmax) / (2.0 * b) + (vmax * vmax) / (2.0 * b);
-    return (v0 - vmax) / b + vmax / b + (dist - d_used) / vmax;
-  };
-  if (d2 <= 1e-24) return one_d(robot.velocity.norm(), 0.0);
-  const double d = std::sqrt(d2);
-  const double denom = d > 1e-30 ? d : 1e-30;
-  const double ex = qx / denom, ey = qy / denom;
-  const double va = robot.velocity.x * ex + robot.velocity.y * ey;
-  const double vc = robot.velocity.x * ey - robot.velocity.y * ex;
-  const double t_along = one_d(va, d > 0.0 ? d : 0.0);
-  const double t_cross = std::fabs(vc) / b;
-  return t_along > t_cross ? t_along : t_cross;
+  return pp::arrival_time(robot.position.x, robot.position.y, robot.velocity.x, robot.velocity.y,
+                          target.x, target.y, limits.max_accel, limits.max_decel,
+                          limits.max_speed)
+      .v;
+}
+
+double arrival_time_with_buffer(const RobotState& robot, Vec2 target, const MotionLimits& limits,
+                                double buffer) {
+  check_nonneg(buffer, "arrival_time_with_buffer: buffer must be >= 0");
+  return arrival_time(robot, target, limits) + buffer;
+}
+
+TrajectorySamples TrajectorySamples::build(const BallTrajectory& traj, double dt) {
+  if (!(dt > 0.0)) throw domain_error("trajectory sampling requires dt > 0");
+  TrajectorySamples s;
+  s.dt = dt;
+  const int n = static_cast<int>(std::floor(traj.stop_time / dt + 1e-9)) + 1;  // samples 0..k_last
+  s.ts.reserve(static_cast<size_t>(n));
+  s.ss.reserve(static_cast<size_t>(n));
+  for (int k = 0; k < n; ++k) {
+    s.ts.push_back(k * dt);
+    s.ss.push_back(traj.distance_at(s.ts.back()));
+  }
+  return s;
+}
+
+std::optional<double> ray_exit_distance(const FieldGeometry& field, Vec2 origin, Vec2 u) {
+  const double s = pp::ray_exit_distance(field.length, field.width, origin.x, origin.y, u.x, u.y).v;
+  if (std::isnan(s)) return std::nullopt;  // origin outside the field
+  return s;
 }
 
 // ---- interception, possession, shot, free kick (GPU via the C-ABI) ---------------

@@ -1440,6 +1440,48 @@ pp_status pp_score_running_points(pp_ctx* ctx, const pp_world* world, const pp_p
   return PP_OK;
 }
 
+pp_status pp_guard_points(pp_ctx* ctx, const pp_world* world, const pp_motion_limits* limits,
+                          double cap, int64_t n, const double* px, const double* py,
+                          double* guard_pq, double* guard_time, uint8_t* ok_out) {
+  if (!ctx || !world || !limits) return fail(ctx, PP_INTERNAL, "null argument");
+  ctx->err.clear();
+  if (!(cap > 0.0) || !std::isfinite(cap))
+    return fail(ctx, PP_DOMAIN, "guard time cap must be positive");
+  if (n == 0) return PP_OK;
+  if (n < 0 || !px || !py) return fail(ctx, PP_INTERNAL, "bad point arrays");
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  pp_params p;
+  pp_params_default(&p);
+  p.motion_theirs = *limits;
+  p.thresholds.guard_time_cap = cap;
+  pp::RunParams R;
+  std::memset(&R, 0, sizeof(R));
+  fill_run_common(*world, p, R);
+  std::vector<double> in(2 * static_cast<size_t>(n));
+  std::memcpy(in.data(), px, n * 8);
+  std::memcpy(in.data() + n, py, n * 8);
+  PP_CUDA_TRY(ctx, ctx->scratch_in.reserve(ctx->stream, in.size() * 8));
+  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(ctx->stream, 6 * static_cast<size_t>(n) * 8));
+  cudaStream_t s = ctx->stream;
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->scratch_in.p, in.data(), in.size() * 8,
+                                   cudaMemcpyHostToDevice, s));
+  const double* d = static_cast<const double*>(ctx->scratch_in.p);
+  pp::guard_points_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, s>>>(
+      R, n, d, d + n, static_cast<double*>(ctx->scratch_out.p));
+  PP_CUDA_TRY(ctx, cudaGetLastError());
+  std::vector<double> o(6 * static_cast<size_t>(n));
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(o.data(), ctx->scratch_out.p, o.size() * 8,
+                                   cudaMemcpyDeviceToHost, s));
+  PP_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < n; ++i) {
+    if (ok_out) ok_out[i] = o[6 * i] != 0.0;
+    if (guard_pq)
+      for (int k = 0; k < 4; ++k) guard_pq[4 * i + k] = o[6 * i + 1 + k];
+    if (guard_time) guard_time[i] = o[6 * i + 5];
+  }
+  return PP_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Batched frames (C5): raw worlds staged on the device, compact summaries.
 

@@ -81,20 +81,13 @@ __device__ __forceinline__ xd entry_param(xd bx0, xd bx1, xd by0, xd by1, xd ax,
   return t_enter.v > 0.0 ? t_enter : xd(0.0);
 }
 
-// score_running_point (offball.cpp:176-201); false where it would throw.
-__device__ __forceinline__ bool score_running_point(const RunParams& R, xd x, xd y, double* score,
-                                                    double* feat) {
+// guard_points + guard_time (offball.cpp:125-174) for a point outside the
+// area's interior; gpq (optional) receives P.x, P.y, Q.x, Q.y.
+__device__ __forceinline__ xd guard_time_at(const RunParams& R, xd x, xd y, double* gpq) {
   const xd hl = xd(0.5) * xd(R.L);
-  if (!(x.v >= 0.0 && x <= hl && xfabs(y) <= xd(0.5) * xd(R.W))) return false;
-  // strictly_in_their_defense_area -> guard_points throws (offball.cpp:126-128)
   const xd dx0 = hl - xd(R.dd);
   const xd hdw = xd(0.5) * xd(R.dw);
-  if (x > dx0 && x < hl && y > -hdw && y < hdw) return false;
   const xd gx = hl;
-  const xd dist_goal = dist2d(x, y, gx, 0.0);
-  const xd dist_ball = dist2d(x, y, R.ball_x, R.ball_y);
-  const xd angle = atan2(xfabs(y - xd(0.0)).v, (gx - x).v);
-  // guard_points / guard_time (offball.cpp:125-174)
   const xd ghh = xd(0.5) * xd(R.gw);
   const xd tp = entry_param(dx0, hl, -hdw, hdw, x, y, gx, ghh);
   const xd tq = entry_param(dx0, hl, -hdw, hdw, x, y, gx, -ghh);
@@ -122,7 +115,29 @@ __device__ __forceinline__ bool score_running_point(const RunParams& R, xd x, xd
   } else {
     total = xd(2.0) * cap;
   }
-  const xd guard = total < cap ? total : cap;
+  if (gpq) {
+    gpq[0] = gpx.v;
+    gpq[1] = gpy.v;
+    gpq[2] = gqx.v;
+    gpq[3] = gqy.v;
+  }
+  return total < cap ? total : cap;
+}
+
+// score_running_point (offball.cpp:176-201); false where it would throw.
+__device__ __forceinline__ bool score_running_point(const RunParams& R, xd x, xd y, double* score,
+                                                    double* feat) {
+  const xd hl = xd(0.5) * xd(R.L);
+  if (!(x.v >= 0.0 && x <= hl && xfabs(y) <= xd(0.5) * xd(R.W))) return false;
+  // strictly_in_their_defense_area -> guard_points throws (offball.cpp:126-128)
+  const xd dx0 = hl - xd(R.dd);
+  const xd hdw = xd(0.5) * xd(R.dw);
+  if (x > dx0 && x < hl && y > -hdw && y < hdw) return false;
+  const xd gx = hl;
+  const xd dist_goal = dist2d(x, y, gx, 0.0);
+  const xd dist_ball = dist2d(x, y, R.ball_x, R.ball_y);
+  const xd angle = atan2(xfabs(y - xd(0.0)).v, (gx - x).v);
+  const xd guard = guard_time_at(R, x, y, nullptr);
   const xd exposure = dist_ball.v > R.nearest_opp ? xd(1.0) : xd(0.0);
   const xd len = R.len_upper;
   const xd s = xd(R.w_dg) * -clamp01(dist_goal / len) + xd(R.w_db) * clamp01(dist_ball / len) +
@@ -150,6 +165,26 @@ __global__ void __launch_bounds__(256) run_points_kernel(RunParams R, int64_t n,
   out7[7 * q] = ok ? 1.0 : 0.0;
   out7[7 * q + 1] = score;
   for (int k = 0; k < 5; ++k) out7[7 * q + 2 + k] = feat[k];
+}
+
+// guard_points / guard_time at explicit points (thread per point, any point
+// of the plane); out6 = ok, P.x, P.y, Q.x, Q.y, guard time.  ok = 0 where the
+// reference throws (strictly inside the defense area, offball.cpp:126-128).
+__global__ void __launch_bounds__(256) guard_points_kernel(RunParams R, int64_t n,
+                                                          const double* __restrict__ px,
+                                                          const double* __restrict__ py,
+                                                          double* __restrict__ out6) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const xd x = px[q], y = py[q];
+  const xd hl = xd(0.5) * xd(R.L);
+  const xd hdw = xd(0.5) * xd(R.dw);
+  const bool inside = x > hl - xd(R.dd) && x < hl && y > -hdw && y < hdw;
+  double gpq[4] = {0.0, 0.0, 0.0, 0.0};
+  const xd t = inside ? xd(0.0) : guard_time_at(R, x, y, gpq);
+  out6[6 * q] = inside ? 0.0 : 1.0;
+  for (int k = 0; k < 4; ++k) out6[6 * q + 1 + k] = gpq[k];
+  out6[6 * q + 5] = t.v;
 }
 
 struct RunOut {

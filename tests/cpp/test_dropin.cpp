@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <optional>
 #include <random>
 #include <string>
 #include <vector>
@@ -304,9 +305,116 @@ void test_batch() {
   check(ok, "best_pass_batch == run_dpps + best_pass per frame");
 }
 
+// best_pass after run_dpps is served from the fused summary; it must equal
+// the re-scoring path (forced by an input that no longer matches the run)
+// and must not serve a stale result for an edited grid.
+void test_best_pass_fused() {
+  std::mt19937_64 rng(0xBE57);
+  const PlannerConfig cfg;
+  PlannerConfig cfg2 = cfg;
+  cfg2.thresholds.drag_v_min = 1.5;  // not an input of score_pass: forces the re-score path
+  int bad = 0;
+  for (int i = 0; i < 12; ++i) {
+    const WorldState w = random_world(rng, 8, 8);
+    const SearchGrid g;
+    const CandidateGrid grid = run_dpps(w, w.ours[0].id, g, cfg, 8);
+    for (const std::optional<KickType> only :
+         {std::optional<KickType>{}, std::optional<KickType>{KickType::flat},
+          std::optional<KickType>{KickType::chip}}) {
+      const auto fused = best_pass(grid, w, cfg, only);
+      const auto rescored = best_pass(grid, w, cfg2, only);
+      if (fused.has_value() != rescored.has_value()) {
+        ++bad;
+      } else if (fused) {
+        bad += fused->score != rescored->score ||
+               fused->candidate.dir_index != rescored->candidate.dir_index ||
+               fused->candidate.power_index != rescored->candidate.power_index ||
+               fused->candidate.kick_type != rescored->candidate.kick_type ||
+               fused->features.shoot_angle_at_receive !=
+                   rescored->features.shoot_angle_at_receive;
+      }
+    }
+    // an edited grid is re-scored: dropping the winner changes the answer
+    const auto best = best_pass(grid, w, cfg);
+    if (best) {
+      CandidateGrid edited = grid;
+      const int slot = best->candidate.kick_type == KickType::flat ? 0 : 1;
+      PassCandidate& c = edited.cells[static_cast<size_t>(
+          edited.cell_index(slot, best->candidate.dir_index, best->candidate.power_index))];
+      c.feasible = false;
+      const auto next = best_pass(edited, w, cfg);
+      bad += next.has_value() && next->candidate.dir_index == best->candidate.dir_index &&
+             next->candidate.power_index == best->candidate.power_index &&
+             next->candidate.kick_type == best->candidate.kick_type;
+      for (auto& cell : edited.cells) cell.feasible = false;
+      bad += best_pass(edited, w, cfg).has_value();
+    }
+  }
+  check(bad == 0, "fused best_pass == re-scored best_pass; edited grids re-scored (" +
+                      std::to_string(bad) + " bad)");
+}
+
+// Reference API entry points outside the search (ball_model.hpp:68-81,
+// motion.hpp:25, intercept.hpp:25-37, offball.hpp:72-75).
+void test_reference_entry_points() {
+  const BallModelParams bp;
+  const auto traj = BallTrajectory::chip_kick({0.5, -0.25}, {3.0, 4.0}, 5.0, bp);
+  const BallSample s = ball_state_at(traj, 0.4);
+  check(s.position == traj.position_at(0.4) && s.speed == traj.speed_at(0.4) &&
+            s.airborne == traj.airborne_at(0.4),
+        "ball_state_at");
+  bool threw = false;
+  check(category_of([&] { (void)ball_state_at(traj, -1.0); }, &threw) == ErrorCategory::domain &&
+            threw,
+        "ball_state_at(t < 0) -> domain_error");
+  check(category_of([&] { (void)travel_time_to_distance(traj, std::nan("")); }, &threw) ==
+                ErrorCategory::domain &&
+            threw,
+        "travel_time_to_distance(NaN) -> domain_error");
+  check(travel_time_to_distance(traj, 1.0) == traj.travel_time_to_distance(1.0) &&
+            !time_of_first_interceptable_point(traj, 0.5 * traj.interceptable_from) &&
+            !travel_time_to_distance(traj, 2.0 * traj.stop_distance),
+        "free travel_time_to_distance / time_of_first_interceptable_point");
+  RobotState r;
+  r.position = {1.0, 2.0};
+  r.velocity = {0.5, -1.0};
+  const MotionLimits lim;
+  check(arrival_time_with_buffer(r, {3.0, -1.0}, lim, 0.3) ==
+            arrival_time(r, {3.0, -1.0}, lim) + 0.3,
+        "arrival_time_with_buffer");
+  check(category_of([&] { (void)arrival_time_with_buffer(r, {0, 0}, lim, -0.1); }, &threw) ==
+                ErrorCategory::domain &&
+            threw,
+        "arrival_time_with_buffer(buffer < 0) -> domain_error");
+  const auto samples = TrajectorySamples::build(traj, 1.0 / 60.0);
+  bool ok = samples.count() == static_cast<int>(std::floor(traj.stop_time * 60.0 + 1e-9)) + 1;
+  for (int k = 0; ok && k < samples.count(); ++k)
+    ok = samples.ts[k] == k * (1.0 / 60.0) && samples.ss[k] == traj.distance_at(samples.ts[k]);
+  check(ok, "TrajectorySamples::build");
+  const FieldGeometry f;
+  const auto ex = ray_exit_distance(f, {0.0, 0.0}, {1.0, 0.0});
+  check(ex && *ex == 6.0 && !ray_exit_distance(f, {7.0, 0.0}, {1.0, 0.0}), "ray_exit_distance");
+  // guard points lie on the area boundary, on the segments to the posts
+  const auto [gp, gq] = guard_points(f, {2.0, 1.0});
+  check(std::fabs(gp.x - 4.2) < 1e-12 && std::fabs(gq.x - 4.2) < 1e-12 && gp.y > gq.y,
+        "guard_points on the area's front edge");
+  check(category_of([&] { (void)guard_points(f, {5.0, 0.0}); }, &threw) ==
+                ErrorCategory::domain &&
+            threw,
+        "guard_points inside the area -> domain_error");
+  WorldState w;
+  check(guard_time({2.0, 1.0}, w, lim) == 10.0, "guard_time with no opponents = cap");
+  check(category_of([&] { (void)guard_time({2.0, 1.0}, w, lim, 0.0); }, &threw) ==
+                ErrorCategory::domain &&
+            threw,
+        "guard_time(cap <= 0) -> domain_error");
+}
+
 }  // namespace
 
 int main() {
+  test_best_pass_fused();
+  test_reference_entry_points();
   test_tables();
   test_grid_vs_oracle();
   test_kicker_never_aggregated();
