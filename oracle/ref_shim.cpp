@@ -676,6 +676,26 @@ int ref_guard_points(const pp_world* world, const pp_motion_limits* limits, doub
   });
 }
 
+// CSV reader -> writer round trip of the reference (csv.cpp): kind 0 = grid,
+// 1 = pass heat map, 2 = run heat map.  The output is the rewritten text, or
+// "ERROR <category>: <message>" when the reader throws.
+int64_t ref_csv_roundtrip(int32_t kind, const char* text, char* buf, size_t len) {
+  std::string out;
+  try {
+    const std::string in(text);
+    if (kind == 0) {
+      out = grid_to_csv(grid_from_csv(in));
+    } else if (kind == 1) {
+      out = heatmap_to_csv(heatmap_from_csv(in));
+    } else {
+      out = run_heatmap_to_csv(run_heatmap_from_csv(in));
+    }
+  } catch (const Error& e) {
+    out = std::string("ERROR ") + category_name(e.category()) + ": " + e.what();
+  }
+  return put_text(out, buf, len);
+}
+
 // `passplan plan --out` CSV of one frame (passplan_main.cpp:89, csv.cpp:85-114).
 // Returns the text length (buf gets a NUL-terminated copy, truncated to len).
 int64_t ref_grid_csv(const pp_world* world, const pp_params* params, int32_t kicker_id,

@@ -72,7 +72,7 @@ def nlohmann_include() -> str:
 def build_dropin(force: bool = False) -> str:
     """lib/libpassplan.so: the reference's C++ API (include/passplan/) over the
     C-ABI, plus its CSV / JSON file formats."""
-    srcs = [os.path.join(CSRC, f) for f in ("passplan_dropin.cpp", "passplan_io.cpp")]
+    srcs = [os.path.join(CSRC, f) for f in ("passplan_dropin.cpp", "passplan_io.cpp", "passplan_csv.cpp")]
     hdrs = [os.path.join(ROOT, "include", "passplan", f)
             for f in os.listdir(os.path.join(ROOT, "include", "passplan"))]
     if force or _stale(DROPIN_LIB, srcs + [LIB] + hdrs):
@@ -113,6 +113,21 @@ def build_cpp_tests(force: bool = False) -> str:
               "-I", os.path.join(ROOT, "include"), src, obj, "-o", CPP_TEST,
               "-L", LIB_DIR, "-lpassplan", "-lpassplan_b200", f"-Wl,-rpath,{LIB_DIR}", "-lm"])
     return CPP_TEST
+
+
+CSV_TOOL = os.path.join(ROOT, "tests", "cpp", "build", "csv_roundtrip")
+
+
+def build_csv_tool(force: bool = False) -> str:
+    """tests/cpp/build/csv_roundtrip: CPU driver of the drop-in's CSV readers
+    and writers (tests/test_csv_cpu.py)."""
+    src = os.path.join(ROOT, "tests", "cpp", "csv_roundtrip.cpp")
+    os.makedirs(os.path.dirname(CSV_TOOL), exist_ok=True)
+    if force or _stale(CSV_TOOL, [src, DROPIN_LIB]):
+        _run([shutil.which("g++") or "g++", "-std=c++20", "-O2", "-ffp-contract=off",
+              "-I", os.path.join(ROOT, "include"), src, "-o", CSV_TOOL,
+              "-L", LIB_DIR, "-lpassplan", "-lpassplan_b200", f"-Wl,-rpath,{LIB_DIR}"])
+    return CSV_TOOL
 
 
 REF_ACCEPTANCE = os.path.join(ROOT, "tests", "cpp", "build", "ref_acceptance")
@@ -159,6 +174,7 @@ def build_all(force: bool = False) -> None:
     build_cli(force=force)
     build_checkers()
     build_cpp_tests(force=force)
+    build_csv_tool(force=force)
     build_ref_acceptance(force=force)
 
 

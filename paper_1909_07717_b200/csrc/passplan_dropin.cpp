@@ -291,30 +291,17 @@ void PlannerConfig::validate() const {
   if (pp_params_validate(&p, msg, sizeof(msg)) != PP_OK) throw config_error(msg);
 }
 
-std::vector<Vec2> direction_table(int n) {
+std::vector<Vec2> direction_table(int n) {  // dpps.cpp:30-48 via pp_math.hpp
+  std::vector<double> xy(2 * static_cast<size_t>(n));
+  pp::direction_table_xy(n, xy.data());
   std::vector<Vec2> dirs(static_cast<size_t>(n));
-  for (int k = 0; k <= n / 2; ++k) {
-    const double theta = direction_angle(k, n);
-    double c = std::cos(theta), s = std::sin(theta);
-    if (k == 0) {
-      c = -1.0;
-      s = 0.0;
-    }
-    dirs[k] = {c, s};
-    const int m = (n - k) % n;
-    if (m != k) dirs[m] = {c, -s};
-  }
+  for (int k = 0; k < n; ++k) dirs[static_cast<size_t>(k)] = {xy[2 * k], xy[2 * k + 1]};
   return dirs;
 }
 
-std::vector<double> power_table(int n, double power_min, double power_max) {
+std::vector<double> power_table(int n, double power_min, double power_max) {  // dpps.cpp:50-62
   std::vector<double> p(static_cast<size_t>(n));
-  if (n == 1) {
-    p[0] = power_min;
-    return p;
-  }
-  const double span = power_max - power_min;
-  for (int j = 0; j < n; ++j) p[j] = power_min + (j * span) / (n - 1);
+  for (int j = 0; j < n; ++j) p[static_cast<size_t>(j)] = pp::power_at(j, n, power_min, power_max).v;
   return p;
 }
 

@@ -1,11 +1,8 @@
-// passplan_io.cpp -- the drop-in's file formats: the reference's CSV outputs
-// (csv.hpp / csv.cpp:70-295) and its JSON world snapshots and planner configs
-// (snapshot.cpp, config.cpp:14-241).  Host code, part of lib/libpassplan.so.
-//
-// The CSV writers reproduce the reference byte for byte (%.17g, "never" for
-// +inf, fixed headers, '\n' line ends); tests/test_gpu_cli.py compares the
-// CLI's files with the reference's own.  JSON uses the same header-only
-// nlohmann/json the reference builds against.
+// passplan_io.cpp -- the drop-in's JSON formats: world snapshots and planner
+// configs (reference snapshot.cpp, config.cpp:14-241), with the same keys,
+// type checks, unknown-key errors and error categories, on the same
+// header-only nlohmann/json the reference builds against.  The CSV formats
+// are in passplan_csv.cpp.  Host code, part of lib/libpassplan.so.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -23,258 +20,10 @@
 
 namespace passplan {
 
+// ---- JSON world snapshots (snapshot.cpp) ----------------------------------------
 namespace {
 
 using nlohmann::json;
-
-constexpr const char* kGridHeader =
-    "kick_type,dir_index,power_index,angle,power,our_id,our_time,opp_id,opp_time,"
-    "receive_x,receive_y,feasible";
-constexpr const char* kHeatHeader = "x,y,value";
-constexpr const char* kRunHeader = "x,y,dist_goal,dist_ball,angle_goal,guard_time,exposure,score";
-
-// Lines without their '\n' (and a trailing '\r'); empty lines are skipped.
-std::vector<std::string> lines_of(const std::string& text) {
-  std::vector<std::string> out;
-  std::string cur;
-  std::istringstream in(text);
-  while (std::getline(in, cur)) {
-    if (!cur.empty() && cur.back() == '\r') cur.pop_back();
-    if (!cur.empty()) out.push_back(cur);
-  }
-  return out;
-}
-
-std::vector<std::string> fields_of(const std::string& line) {
-  std::vector<std::string> out(1);
-  for (char ch : line) {
-    if (ch == ',') {
-      out.emplace_back();
-    } else {
-      out.back().push_back(ch);
-    }
-  }
-  return out;
-}
-
-[[noreturn]] void row_error(size_t line, const std::string& what) {
-  throw schema_error("csv line " + std::to_string(line) + ": " + what);
-}
-
-int int_field(const std::string& f, size_t line) {
-  if (f.empty()) row_error(line, "empty integer field");
-  char* end = nullptr;
-  const long v = std::strtol(f.c_str(), &end, 10);
-  if (end != f.c_str() + f.size()) row_error(line, "bad integer '" + f + "'");
-  return static_cast<int>(v);
-}
-
-double num_field(const std::string& f, size_t line) {
-  try {
-    return parse_double_field(f);
-  } catch (const Error& e) {
-    row_error(line, e.what());
-  }
-}
-
-void append_num(std::string* out, double v) {
-  *out += format_double(v);
-}
-
-}  // namespace
-
-std::string format_double(double v) {
-  if (std::isinf(v) && v > 0.0) return "never";
-  char buf[40];
-  std::snprintf(buf, sizeof(buf), "%.17g", v);
-  return buf;
-}
-
-double parse_double_field(const std::string& field) {
-  if (field == "never") return kNever;
-  if (field.empty()) throw schema_error("empty number field");
-  char* end = nullptr;
-  const double v = std::strtod(field.c_str(), &end);
-  if (end != field.c_str() + field.size()) throw schema_error("bad number '" + field + "'");
-  return v;
-}
-
-std::string grid_to_csv(const CandidateGrid& g) {
-  std::string out = kGridHeader;
-  out += '\n';
-  out.reserve(out.size() + g.cells.size() * 140);
-  for (const PassCandidate& c : g.cells) {
-    out += c.kick_type == KickType::flat ? "flat," : "chip,";
-    out += std::to_string(c.dir_index) + ',' + std::to_string(c.power_index) + ',';
-    append_num(&out, direction_angle(c.dir_index, g.grid.n_directions));
-    out += ',';
-    append_num(&out, g.powers[static_cast<size_t>(c.power_index)]);
-    out += ',' + std::to_string(c.our_id) + ',';
-    append_num(&out, c.our_time);
-    out += ',' + std::to_string(c.opp_id) + ',';
-    append_num(&out, c.opp_time);
-    out += ',';
-    append_num(&out, c.receive_point.x);
-    out += ',';
-    append_num(&out, c.receive_point.y);
-    out += c.feasible ? ",1\n" : ",0\n";
-  }
-  return out;
-}
-
-CandidateGrid grid_from_csv(const std::string& text) {
-  const std::vector<std::string> lines = lines_of(text);
-  if (lines.empty()) throw schema_error("csv: empty input");
-  if (lines[0] != kGridHeader) throw schema_error("csv line 1: unexpected header");
-  struct Row {
-    PassCandidate cell;
-    double power;
-  };
-  std::vector<Row> rows;
-  int n_dirs = 0, n_powers = 0;
-  bool has_flat = false, has_chip = false;
-  for (size_t i = 1; i < lines.size(); ++i) {
-    const size_t ln = i + 1;
-    const std::vector<std::string> f = fields_of(lines[i]);
-    if (f.size() != 12) row_error(ln, "expected 12 fields");
-    Row r{};
-    if (f[0] == "flat") {
-      r.cell.kick_type = KickType::flat;
-      has_flat = true;
-    } else if (f[0] == "chip") {
-      r.cell.kick_type = KickType::chip;
-      has_chip = true;
-    } else {
-      row_error(ln, "unknown kick type '" + f[0] + "'");
-    }
-    r.cell.dir_index = int_field(f[1], ln);
-    r.cell.power_index = int_field(f[2], ln);
-    num_field(f[3], ln);  // the angle follows from dir_index: checked only
-    r.power = num_field(f[4], ln);
-    r.cell.our_id = int_field(f[5], ln);
-    r.cell.our_time = num_field(f[6], ln);
-    r.cell.opp_id = int_field(f[7], ln);
-    r.cell.opp_time = num_field(f[8], ln);
-    r.cell.receive_point = {num_field(f[9], ln), num_field(f[10], ln)};
-    if (f[11] != "0" && f[11] != "1") row_error(ln, "feasible must be 0 or 1");
-    r.cell.feasible = f[11] == "1";
-    if (r.cell.dir_index < 0 || r.cell.power_index < 0) row_error(ln, "negative index");
-    n_dirs = std::max(n_dirs, r.cell.dir_index + 1);
-    n_powers = std::max(n_powers, r.cell.power_index + 1);
-    rows.push_back(r);
-  }
-  if (rows.empty()) throw schema_error("csv: no data rows");
-  CandidateGrid g;
-  g.grid.n_directions = n_dirs;
-  g.grid.n_powers = n_powers;
-  g.grid.flat = has_flat;
-  g.grid.chip = has_chip;
-  g.kick_types = g.grid.kick_types();
-  g.directions = direction_table(n_dirs);
-  g.powers.assign(static_cast<size_t>(n_powers), 0.0);
-  const size_t expected = g.kick_types.size() * size_t(n_dirs) * size_t(n_powers);
-  if (rows.size() != expected)
-    throw schema_error("csv: " + std::to_string(rows.size()) + " rows, expected " +
-                       std::to_string(expected));
-  g.cells.assign(expected, PassCandidate{});
-  for (const Row& r : rows) {
-    const int slot = (r.cell.kick_type == KickType::chip && has_flat) ? 1 : 0;
-    g.cells[static_cast<size_t>(g.cell_index(slot, r.cell.dir_index, r.cell.power_index))] = r.cell;
-    g.powers[static_cast<size_t>(r.cell.power_index)] = r.power;
-  }
-  g.grid.power_min = g.powers.front();
-  g.grid.power_max = g.powers.back();
-  return g;
-}
-
-std::string heatmap_to_csv(const std::vector<HeatPoint>& points) {
-  std::string out = std::string(kHeatHeader) + '\n';
-  for (const HeatPoint& p : points) {
-    append_num(&out, p.point.x);
-    out += ',';
-    append_num(&out, p.point.y);
-    out += ',';
-    append_num(&out, p.value);
-    out += '\n';
-  }
-  return out;
-}
-
-std::vector<HeatPoint> heatmap_from_csv(const std::string& text) {
-  const std::vector<std::string> lines = lines_of(text);
-  if (lines.empty() || lines[0] != kHeatHeader)
-    throw schema_error("csv line 1: expected x,y,value");
-  std::vector<HeatPoint> out;
-  for (size_t i = 1; i < lines.size(); ++i) {
-    const std::vector<std::string> f = fields_of(lines[i]);
-    if (f.size() != 3) row_error(i + 1, "expected 3 fields");
-    out.push_back({{num_field(f[0], i + 1), num_field(f[1], i + 1)}, num_field(f[2], i + 1)});
-  }
-  return out;
-}
-
-std::string run_heatmap_to_csv(const std::vector<RunHeatRow>& rows) {
-  std::string out = std::string(kRunHeader) + '\n';
-  for (const RunHeatRow& r : rows) {
-    const double v[8] = {r.point.x,
-                         r.point.y,
-                         r.features.dist_to_goal,
-                         r.features.dist_to_ball,
-                         r.features.angle_to_goal,
-                         r.features.guard_time,
-                         r.features.defense_exposure,
-                         r.score};
-    for (int k = 0; k < 8; ++k) {
-      if (k) out += ',';
-      append_num(&out, v[k]);
-    }
-    out += '\n';
-  }
-  return out;
-}
-
-std::vector<RunHeatRow> run_heatmap_from_csv(const std::string& text) {
-  const std::vector<std::string> lines = lines_of(text);
-  if (lines.empty() || lines[0] != kRunHeader)
-    throw schema_error("csv line 1: unexpected run-heatmap header");
-  std::vector<RunHeatRow> out;
-  for (size_t i = 1; i < lines.size(); ++i) {
-    const std::vector<std::string> f = fields_of(lines[i]);
-    if (f.size() != 8) row_error(i + 1, "expected 8 fields");
-    double v[8];
-    for (int k = 0; k < 8; ++k) v[k] = num_field(f[k], i + 1);
-    RunHeatRow r;
-    r.point = {v[0], v[1]};
-    r.features = {v[2], v[3], v[4], v[5], v[6]};
-    r.score = v[7];
-    out.push_back(r);
-  }
-  return out;
-}
-
-std::string read_text_file(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw config_error("cannot open " + path);
-  std::ostringstream ss;
-  ss << in.rdbuf();
-  return ss.str();
-}
-
-void write_text_file(const std::string& path, const std::string& text) {
-  const std::string tmp = path + ".tmp";
-  {
-    std::ofstream out(tmp, std::ios::binary | std::ios::trunc);
-    if (!out) throw config_error("cannot write " + tmp);
-    out << text;
-    if (!out.flush()) throw config_error("short write to " + tmp);
-  }
-  std::error_code ec;
-  std::filesystem::rename(tmp, path, ec);
-  if (ec) throw config_error("cannot rename " + tmp + " to " + path + ": " + ec.message());
-}
-
-// ---- JSON world snapshots (snapshot.cpp) ----------------------------------------
-namespace {
 
 // Checks an object's keys: all of `need` present, nothing outside need+opt.
 void check_keys(const json& o, const std::string& at, std::initializer_list<const char*> need,

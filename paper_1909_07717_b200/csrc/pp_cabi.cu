@@ -300,22 +300,7 @@ bool validate_grid(const pp_search_grid& g, std::string* why) {
 // direction_table (dpps.cpp:30-48) with the host libm, bit-identical.
 std::vector<double> direction_table(int n) {
   std::vector<double> xy(2 * static_cast<size_t>(n));
-  for (int k = 0; k <= n / 2; ++k) {
-    const double theta = -kPi + k * (2.0 * kPi / n);
-    double c = std::cos(theta);
-    double s = std::sin(theta);
-    if (k == 0) {
-      c = -1.0;
-      s = 0.0;
-    }
-    xy[2 * k] = c;
-    xy[2 * k + 1] = s;
-    const int m = (n - k) % n;
-    if (m != k) {
-      xy[2 * m] = c;
-      xy[2 * m + 1] = -s;
-    }
-  }
+  pp::direction_table_xy(n, xy.data());
   return xy;
 }
 
@@ -543,10 +528,7 @@ cudaError_t ensure_tables(pp_ctx* ctx, pp::DevParams* P) {
     for (int s = 0; s < P->n_kt; ++s) {
       const bool chip = (s == 0 ? P->kt_chip0 : P->kt_chip1) != 0;
       for (int pw = 0; pw < P->n_pows; ++pw) {
-        xd speed = P->power_min;  // power_table, dpps.cpp:50-62
-        if (P->n_pows > 1)
-          speed = xd(P->power_min) + (xd(double(pw)) * (xd(P->power_max) - xd(P->power_min))) /
-                                         xd(double(P->n_pows - 1));
+        const xd speed = pp::power_at(pw, P->n_pows, P->power_min, P->power_max);
         const pp::Traj tr = pp::resolve_kick(speed, chip, slide, roll, P->ratio, P->chip_frac);
         pp::PowRow& r = rows[static_cast<size_t>(s) * P->n_pows + pw];
         r.speed = tr.speed.v;
@@ -1989,11 +1971,7 @@ pp_status pp_plan_free_kick(pp_ctx* ctx, const pp_world* world, const pp_params*
   if (target->power_index < 0 || target->power_index >= g.n_powers)
     return fail(ctx, PP_DOMAIN,
                 "plan_free_kick: candidate power index outside the configured grid");
-  // power_table (dpps.cpp:50-62)
-  xd power = g.power_min;
-  if (g.n_powers != 1)
-    power = xd(g.power_min) + (xd(double(target->power_index)) * (xd(g.power_max) - xd(g.power_min))) /
-                                  xd(double(g.n_powers - 1));
+  const xd power = pp::power_at(target->power_index, g.n_powers, g.power_min, g.power_max);
   pp_kick k{world->ball_px, world->ball_py, (xd(target->receive_x) - xd(world->ball_px)).v,
             (xd(target->receive_y) - xd(world->ball_py)).v, power.v, target->kick_type == 1 ? 1 : 0,
             0};
