@@ -525,6 +525,7 @@ def run_frame_c2(lib, ctx, args, torch, stream, flush):
     scan_ms, value_ms = C.c_float(), C.c_float()
     lib.pp_dpps_kernel_times(ctx, 50, C.byref(scan_ms), C.byref(value_ms))
     lib.pp_host_free(hblock)
+    cpp_seq = cpp_plan_sequence(max(reps, 200))
     return {"workload": "configs[1]: frame F8 (8v8), 128x64 grid, flat+chip, 16,384 cells, "
                         "262,144 pass evaluations; search + value function + best_pass x3",
             "p50_ms": statistics.median(dev_ms), "p99_ms": float(np.percentile(dev_ms, 99)),
@@ -533,7 +534,24 @@ def run_frame_c2(lib, ctx, args, torch, stream, flush):
             "e2e_h2d_bytes": int(lib.pp_dpps_upload_bytes()), "e2e_d2h_bytes": block_bytes,
             "scan_ms": scan_ms.value, "value_ms": value_ms.value,
             "search_pair_evals_per_s": C2_PAIRS / (scan_ms.value / 1e3),
-            "reps": reps, "l2": "flushed between device-timed reps"}
+            "reps": reps, "l2": "flushed between device-timed reps",
+            "cpp_plan_sequence": cpp_seq}
+
+
+def cpp_plan_sequence(reps):
+    """The reference's plan sequence (run_dpps + best_pass all/flat/chip,
+    passplan_main.cpp:87,102-104) through the C++ drop-in on the same frame:
+    tests/cpp/build/plan_sequence, host-timed p50."""
+    exe = os.path.join(ROOT, "tests", "cpp", "build", "plan_sequence")
+    snap = os.path.join(ROOT, "tests", "golden", "data", "bench_16v16.json")
+    if not os.path.exists(exe):
+        return None
+    try:
+        r = subprocess.run([exe, snap, str(reps)], capture_output=True, text=True, timeout=300)
+        return json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else \
+            {"error": r.stderr.strip()[-300:]}
+    except (OSError, ValueError, subprocess.TimeoutExpired) as e:
+        return {"error": str(e)}
 
 
 def run_extras(lib, ctx):

@@ -130,6 +130,21 @@ def build_csv_tool(force: bool = False) -> str:
     return CSV_TOOL
 
 
+PLAN_SEQ = os.path.join(ROOT, "tests", "cpp", "build", "plan_sequence")
+
+
+def build_plan_sequence(force: bool = False) -> str:
+    """tests/cpp/build/plan_sequence: the reference's plan sequence (run_dpps +
+    best_pass x3) timed through the C++ drop-in (bench.py runs it)."""
+    src = os.path.join(ROOT, "tests", "cpp", "plan_sequence.cpp")
+    os.makedirs(os.path.dirname(PLAN_SEQ), exist_ok=True)
+    if force or _stale(PLAN_SEQ, [src, DROPIN_LIB]):
+        _run([shutil.which("g++") or "g++", "-std=c++20", "-O2", "-ffp-contract=off",
+              "-I", os.path.join(ROOT, "include"), src, "-o", PLAN_SEQ,
+              "-L", LIB_DIR, "-lpassplan", "-lpassplan_b200", f"-Wl,-rpath,{LIB_DIR}"])
+    return PLAN_SEQ
+
+
 REF_ACCEPTANCE = os.path.join(ROOT, "tests", "cpp", "build", "ref_acceptance")
 REF_TESTS = "/root/reference/proj/tests"
 
@@ -175,6 +190,7 @@ def build_all(force: bool = False) -> None:
     build_checkers()
     build_cpp_tests(force=force)
     build_csv_tool(force=force)
+    build_plan_sequence(force=force)
     build_ref_acceptance(force=force)
 
 
