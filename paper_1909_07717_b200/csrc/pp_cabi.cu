@@ -1422,6 +1422,19 @@ pp_status pp_score_running_points(pp_ctx* ctx, const pp_world* world, const pp_p
   return PP_OK;
 }
 
+#ifdef PP_SCAN_STATS
+// Dev variant only (not in the header): read and optionally reset the scan
+// filter statistics (pp_scan.cuh g_scan_stats).
+void pp_debug_scan_stats(unsigned long long* out16, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out16, pp::g_scan_stats, 16 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(pp::g_scan_stats, z, sizeof(z));
+  }
+}
+#endif
+
 pp_status pp_guard_points(pp_ctx* ctx, const pp_world* world, const pp_motion_limits* limits,
                           double cap, int64_t n, const double* px, const double* py,
                           double* guard_pq, double* guard_time, uint8_t* ok_out) {

@@ -406,6 +406,17 @@ __device__ __forceinline__ CellLane cell_window(const FrameDev& F, const DevPara
   return c;
 }
 
+// Dev statistics of the filters (variant build -DPP_SCAN_STATS only; read
+// with pp_debug_scan_stats): sample outcomes, skipped samples, warp steps.
+#ifdef PP_SCAN_STATS
+__device__ unsigned long long g_scan_stats[16];
+#define PP_STAT(i) atomicAdd(&g_scan_stats[i], 1ull)
+#define PP_STATN(i, n) atomicAdd(&g_scan_stats[i], static_cast<unsigned long long>(n))
+#else
+#define PP_STAT(i)
+#define PP_STATN(i, n)
+#endif
+
 // FP32 sample filter outcome (scan_robot / scan_leftovers).
 enum SampleCode { kNone = 0, kRej = 1, kEnd = 2, kCap = 3, kHit = 4, kCand = 5 };
 
@@ -439,8 +450,15 @@ __device__ __forceinline__ SampleF sample_f(const RobotK& rk, float2 uf, const D
 // kHit (certainly feasible), kCand (needs the exact test).
 __device__ __forceinline__ int test_sample(const RobotK& rk, const SampleF& S, int kk,
                                            const TrajF& tf_, int ke_s, int cap_c, int* next) {
-  if (kk >= ke_s) return kEnd;
-  if (kk > cap_c) return kCap;
+  PP_STAT(0);
+  if (kk >= ke_s) {
+    PP_STAT(1);
+    return kEnd;
+  }
+  if (kk > cap_c) {
+    PP_STAT(2);
+    return kCap;
+  }
   if (S.exact) return kCand;
   const float tf = static_cast<float>(kk) * S.dtf;
   const float sf = tf_.distance_at(tf);
@@ -459,15 +477,22 @@ __device__ __forceinline__ int test_sample(const RobotK& rk, const SampleF& S, i
     const float rate = (approach + S.vbf) * S.dtf * 1.0001f;
     const float j = floorf(gap * rcp_ftz(rate) * 0.9999f);
     *next = kk + 1 + (j > 1.f ? (j < 4096.f ? static_cast<int>(j) - 1 : 4095) : 0);
+    PP_STAT(3);
+    PP_STATN(4, *next - kk - 1);
     return kRej;
   }
   if (rk.lb.lower_bound(qxf, qyf, df, inv_d, S.radf) > fmaf(tf, 1.000001f, 1e-6f)) {
     *next = kk + 1;
+    PP_STAT(5);
     return kRej;
   }
   // certainly feasible: arrival <= t with margin (and then the reference's
   // quick reject cannot fire: reach - deff >= vbound t / 2)
-  if (rk.lb.upper_bound(qxf, qyf, df, inv_d, S.radf) < fmaf(tf, 0.999999f, -1e-6f)) return kHit;
+  if (rk.lb.upper_bound(qxf, qyf, df, inv_d, S.radf) < fmaf(tf, 0.999999f, -1e-6f)) {
+    PP_STAT(6);
+    return kHit;
+  }
+  PP_STAT(7);
   return kCand;
 }
 
@@ -584,6 +609,8 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
   const int lane = threadIdx.x & 31;
   const int ke = c.valid ? c.ke : 0;
   int k = scan_start(c, S, F, ri);
+  PP_STAT(10);
+  if (k >= ke) PP_STAT(11);
   const TrajF trf = trf_in;
   int hit = -1;
   bool capped = false;
@@ -597,13 +624,21 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
   volatile int* vcap = cap + team * 32 + lane;
   for (int n_step = 0; n_step < max_steps; ++n_step) {
     const unsigned act = __ballot_sync(0xffffffffu, state == 0);
+#ifdef PP_SCAN_STATS
+    if (lane == 0) {
+      PP_STAT(12);
+      PP_STATN(13, __popc(act));
+    }
+#endif
     if (act == 0u) {
       const bool pend = state == 1;
       if (!__any_sync(0xffffffffu, pend)) break;
       PP_CNT(c_rounds);
       if (pend) {
         PP_CNT(c_exact);
+        PP_STAT(8);
         if (exact_hit(c, F, P, robot_x(F, P, rk, ri), k)) {
+          PP_STAT(9);
           hit = k;
           atomicMin(&cap[team * 32 + lane], k);
           state = 2;
@@ -638,6 +673,7 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
   }
   PP_CNT_FLUSH();
   if (state != 2) {
+    PP_STAT(14);
     *left_k = k;
     return;
   }

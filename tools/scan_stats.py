@@ -1,0 +1,38 @@
+"""Dev tool (GPU box): filter statistics of the scan kernel from the
+-DPP_SCAN_STATS variant (tools/build_variants.sh stats -DPP_SCAN_STATS):
+per (robot, cell) pair, how many samples the FP32 filters tested and how
+each test ended.  PP_LIB_PATH=variants/libpassplan_b200_stats.so
+python tools/scan_stats.py [n_frames]"""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1909_07717_b200 import abi, synthetic  # noqa: E402
+
+NAMES = ["tests", "end", "cap", "reach_rej", "reach_skipped", "lb_rej", "ub_hit", "cand",
+         "exact", "exact_hit", "pairs", "pairs_pruned", "warp_steps", "active_lanes",
+         "to_leftovers", "-"]
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+lib = abi.load_library()
+lib.pp_debug_scan_stats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+lib.pp_debug_scan_stats.restype = None
+ctx = C.c_void_p()
+assert lib.pp_ctx_create(0, C.byref(ctx)) == 0
+p = abi.Params()
+lib.pp_params_default(C.byref(p))
+st = (C.c_ulonglong * 16)()
+for chip in (0, 1):
+    g = abi.SearchGrid(128, 64, 1.0, 6.5, 1, chip)
+    fr, keep = synthetic.as_ctypes(synthetic.c5_frames(0, n))
+    assert lib.pp_batch_upload(ctx, fr, n, None) == 0
+    lib.pp_debug_scan_stats(st, 1)
+    ms = C.c_float()
+    assert lib.pp_batch_run(ctx, C.byref(p), C.byref(g), C.byref(ms)) == 0
+    lib.pp_debug_scan_stats(st, 1)
+    pairs = st[10]
+    print(f"C5 batch {n} frames chip={chip}: pairs {pairs}")
+    for i, nm in enumerate(NAMES[:15]):
+        print(f"  {nm:14s} {st[i]:14d}  per pair {st[i] / pairs:8.3f}")
+    print(f"  SIMT lanes/step {st[13] / max(st[12], 1):.2f}")
