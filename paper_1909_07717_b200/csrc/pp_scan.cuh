@@ -558,6 +558,45 @@ __device__ __forceinline__ void pair_result(const CellLane& c, const DevParams& 
   *code_out = code;
 }
 
+// The scan's own outcome of a finished pair: a hit, capped out, or kNoHit --
+// no sample hit, the rest rule decides (resolved by rest_rule_pass once every
+// robot of the tile is done).
+constexpr int kNoHit = -4;
+__device__ __forceinline__ void pair_outcome(int hit, bool capped, const DevParams& P,
+                                             double* t_out, int* code_out) {
+  *t_out = hit >= 0 ? (xd(double(hit)) * xd(P.dt)).v : CUDART_INF;
+  *code_out = hit >= 0 ? hit : (capped ? -3 : kNoHit);
+}
+
+// The rest rule (dpps.cpp:177-190) for every kNoHit pair of the tile, all
+// threads, after the scan phase.  Skipped -- (+inf, never) -- where a robot
+// of the same team hit strictly before the ball comes to rest: the rest-rule
+// time max(arrival, t_stop) >= t_stop is then later than that hit, so it can
+// neither win nor tie the team's champion (the only robot whose time and id
+// reach the outputs, dpps.cpp:192-213).
+template <class ResT, class ResK>
+__device__ __forceinline__ void rest_rule_pass(const CellLane* cl, const FrameDev& F,
+                                               const DevParams& P, const RobotK* rk_s,
+                                               const int (*cap)[32], ResT res_t, ResK res_k) {
+  for (int e = threadIdx.x; e < F.n_scan * 32; e += blockDim.x) {
+    const int ri = e >> 5, cell = e & 31;
+    if (res_k[ri][cell] != kNoHit) continue;
+    const CellLane& c = cl[cell];
+    const int team = F.scan_slot[ri] >= kTheirs ? 1 : 0;
+    const int k_team = cap[team][cell];
+    double t;
+    int cd;
+    if (k_team != 0x7fffffff && xd(double(k_team)) * xd(P.dt) < c.tr.t_stop) {
+      t = CUDART_INF;
+      cd = -2;
+    } else {
+      pair_result(c, P, robot_x(F, P, rk_s[ri], ri), -1, false, &t, &cd);
+    }
+    res_t[ri][cell] = t;
+    res_k[ri][cell] = cd;
+  }
+}
+
 // First sample worth testing for robot ri on cell c (ke when none):
 // scan_robot's prunes (intercept.cpp:89-113) in FP32 with 1e-3 m of slack --
 // the window is skipped, or the scan starts late, only where every sample
@@ -678,7 +717,7 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
     return;
   }
   *left_k = -1;
-  pair_result(c, P, robot_x(F, P, rk, ri), hit, capped, t_out, code_out);
+  pair_outcome(hit, capped, P, t_out, code_out);
 }
 
 // Scan pairs left over by scan_robot: left[] holds ri << 5 | cell and
@@ -766,10 +805,9 @@ __device__ __forceinline__ void scan_leftovers(const CellLane* cl, const TrajF* 
     if (done) {
       if (o == 0) {
         if (hit >= 0) atomicMin(&cap[team * 32 + cell], hit);
-        const RobotX X = robot_x(F, P, rk, ri);
         double t;
         int cd;
-        pair_result(cl[cell], P, X, hit, capped, &t, &cd);
+        pair_outcome(hit, capped, P, &t, &cd);
         res_t[ri][cell] = t;
         res_k[ri][cell] = cd;
       }
@@ -1058,6 +1096,8 @@ __device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, cons
         __syncthreads();
       }
     }
+    rest_rule_pass(cl, F, P, sm.rk, sm.cap, sm.res_t, sm.res_k);
+    __syncthreads();
     PP_TMARK(1);
     PP_CMARK(0);
 

@@ -239,9 +239,12 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
                                       feat);
     const int64_t c = sm.q_cell[e];
     if (kCells) out.score[c] = static_cast<float>(sc);
-    const int s = sm.q_slot[e];
-    bs[s] = sc;
-    bc[s] = c;
+    // (selects, not a runtime-indexed store: bs/bc stay in registers)
+    const bool s1 = sm.q_slot[e] != 0;
+    bs[0] = s1 ? bs[0] : sc;
+    bc[0] = s1 ? bc[0] : c;
+    bs[1] = s1 ? sc : bs[1];
+    bc[1] = s1 ? c : bc[1];
   }
   PP_MARK(5);
   // The chunk's argmax per kick slot: D3 ran on warp 0 only (m <= 32), so one
@@ -362,8 +365,19 @@ __device__ __forceinline__ void fold_frame(FoldSmem& fs, const Partial* base, in
 // D2  thread per (interval slot, edge): the edge bisection
 // D3  thread per cell: sort + sweep (atan2), score_pass, score map store
 // then the chunk's argmax per kick slot; the last chunk of a frame folds.
+// Register caps (min resident CTAs per SM): the 128-thread batch shape at 6
+// (80 registers: C5 value time 20.8 -> 13.8 ms per 16k frames against the
+// uncapped 158-179), the 256-thread single-frame shape at 2 (128 registers;
+// 3-4 only lengthen the D2 chains).  Measured with tools/variant_*.py.
+#ifndef PP_VALUE_MINB
+#define PP_VALUE_MINB 6
+#endif
+#ifndef PP_VALUE_MINB_WIDE
+#define PP_VALUE_MINB_WIDE 2
+#endif
 template <bool kCells, int kThreads>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, kThreads == kValueThreadsWide ? PP_VALUE_MINB_WIDE
+                                                                          : PP_VALUE_MINB)
     value_kernel(const FrameDev* __restrict__ frames, DevParams P, CellQueue q,
                  FrameCounters* __restrict__ fc, CellOut out, Partial* __restrict__ partials,
                  pp_dpps_summary* __restrict__ summaries, int chunks_per_frame,
