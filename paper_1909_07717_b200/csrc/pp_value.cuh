@@ -381,15 +381,17 @@ __global__ void __launch_bounds__(kThreads, kThreads == kValueThreadsWide ? PP_V
     value_kernel(const FrameDev* __restrict__ frames, DevParams P, CellQueue q,
                  FrameCounters* __restrict__ fc, CellOut out, Partial* __restrict__ partials,
                  pp_dpps_summary* __restrict__ summaries, int chunks_per_frame,
-                 const __grid_constant__ FrameDev fa) {
+                 int ctas_per_frame, const __grid_constant__ FrameDev fa) {
   __shared__ ValueSmem sm;
   __shared__ FoldSmem fs;
-  const int f = blockIdx.x / chunks_per_frame;
-  const int ch = blockIdx.x % chunks_per_frame;
+  const int f = blockIdx.x / ctas_per_frame;
+  const int c0 = blockIdx.x % ctas_per_frame;
   // The frame (copied in before the scan started) and its view heights do
   // not depend on the scan.  Single-frame launches (the wide shape, at most
-  // a wave of CTAs) stage them while the scan's last CTAs still run; large
-  // launches, where most chunk CTAs find no work, only after the check.
+  // a wave of CTAs, one chunk per CTA) stage them while the scan's last CTAs
+  // still run; batches (ctas_per_frame CTAs per frame, each taking chunks
+  // c0, c0 + ctas_per_frame, ... of the frame's queue) only once a CTA has
+  // work.
   constexpr bool kEarly = kThreads == kValueThreadsWide;
   if (kEarly) {
     load_frame(&sm.frame, P.frame_in_arg ? &fa : frames + f);
@@ -402,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, kThreads == kValueThreadsWide ? PP_V
   auto leave = [&]() {
     if (stream && threadIdx.x == 0) {
       __threadfence();
-      if (atomicAdd(&fc[f].value_out, 1u) == static_cast<unsigned>(chunks_per_frame - 1)) {
+      if (atomicAdd(&fc[f].value_out, 1u) == static_cast<unsigned>(ctas_per_frame - 1)) {
         fc[f].tiles_done = 0;
         fc[f].value_out = 0;
       }
@@ -414,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, kThreads == kValueThreadsWide ? PP_V
     // entries are written, or once every tile is done (the last, partial
     // chunk, or a chunk that stays empty).
     if (threadIdx.x == 0) {
-      volatile unsigned* fill = P.chunk_fill + ch;
+      volatile unsigned* fill = P.chunk_fill + c0;
       volatile unsigned* tiles = &fc[f].tiles_done;
       int nq = -1;
       for (unsigned spins = 0;; ++spins) {
@@ -435,13 +437,13 @@ __global__ void __launch_bounds__(kThreads, kThreads == kValueThreadsWide ? PP_V
     }
     __syncthreads();
     if (sm.n_act == -2) return;
-    n_q = sm.n_act < 0 ? (ch + 1) * kChunk : sm.n_act;
+    n_q = sm.n_act < 0 ? (c0 + 1) * kChunk : sm.n_act;
   } else {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // scan grid done and visible
     n_q = static_cast<int>(fc[f].q_count);
   }
   const int n_active_lb = n_q > 0 ? (n_q + kChunk - 1) / kChunk : 1;
-  if (ch >= n_active_lb) {
+  if (c0 >= n_active_lb) {
     leave();
     return;
   }
@@ -450,40 +452,44 @@ __global__ void __launch_bounds__(kThreads, kThreads == kValueThreadsWide ? PP_V
     __syncthreads();
     value_heights(sm, P);
   }
-  const int e0 = ch * kChunk;
-  const int m = n_q - e0 < kChunk ? (n_q - e0 > 0 ? n_q - e0 : 0) : kChunk;
   Partial* base = partials + static_cast<int64_t>(f) * chunks_per_frame;
-  value_chunk<kCells>(sm, P, q, out, f, e0, m, base + ch);
-  if (threadIdx.x == 0) {
-    int n_active = n_active_lb;
-    bool stalled = false;
-    if (stream) {
-      P.chunk_fill[ch] = 0;  // consumed (self-cleaning for the next launch)
-      // the fold needs the final chunk count: wait for the scan's last tile
-      volatile unsigned* tiles = &fc[f].tiles_done;
-      for (unsigned spins = 0; *tiles != static_cast<unsigned>(P.n_tiles); ++spins) {
-        if (spins > kSpinLimit) {
-          stalled = true;
-          break;
+  // (streaming CTAs take exactly one chunk: ctas_per_frame == chunks_per_frame)
+  for (int ch = c0; ch < n_active_lb; ch += ctas_per_frame) {
+    const int e0 = ch * kChunk;
+    const int m = n_q - e0 < kChunk ? (n_q - e0 > 0 ? n_q - e0 : 0) : kChunk;
+    value_chunk<kCells>(sm, P, q, out, f, e0, m, base + ch);
+    if (threadIdx.x == 0) {
+      int n_active = n_active_lb;
+      bool stalled = false;
+      if (stream) {
+        P.chunk_fill[ch] = 0;  // consumed (self-cleaning for the next launch)
+        // the fold needs the final chunk count: wait for the scan's last tile
+        volatile unsigned* tiles = &fc[f].tiles_done;
+        for (unsigned spins = 0; *tiles != static_cast<unsigned>(P.n_tiles); ++spins) {
+          if (spins > kSpinLimit) {
+            stalled = true;
+            break;
+          }
+          __nanosleep(256);
         }
-        __nanosleep(256);
+        __threadfence();
+        const int nq = static_cast<int>(*reinterpret_cast<volatile unsigned*>(&fc[f].q_count));
+        n_active = nq > 0 ? (nq + kChunk - 1) / kChunk : 1;
       }
-      __threadfence();
-      const int nq = static_cast<int>(*reinterpret_cast<volatile unsigned*>(&fc[f].q_count));
-      n_active = nq > 0 ? (nq + kChunk - 1) / kChunk : 1;
+      sm.last = 0;
+      sm.n_act = -2;
+      if (!stalled) {
+        __threadfence();
+        const unsigned prev = atomicAdd(&fc[f].chunks_done, 1u);
+        sm.last = prev == static_cast<unsigned>(n_active - 1);
+        sm.n_act = n_active;
+      }
     }
-    sm.last = 0;
-    sm.n_act = -2;
-    if (!stalled) {
-      __threadfence();
-      const unsigned prev = atomicAdd(&fc[f].chunks_done, 1u);
-      sm.last = prev == static_cast<unsigned>(n_active - 1);
-      sm.n_act = n_active;
-    }
+    __syncthreads();
+    if (sm.n_act == -2) return;  // stalled: no fold (the host reports it)
+    if (sm.last) fold_frame(fs, base, sm.n_act, fc + f, P, summaries ? summaries + f : nullptr, f);
+    __syncthreads();  // (sm reused by the next chunk)
   }
-  __syncthreads();
-  if (sm.n_act == -2) return;  // stalled: no fold (the host reports it)
-  if (sm.last) fold_frame(fs, base, sm.n_act, fc + f, P, summaries ? summaries + f : nullptr, f);
   leave();  // after the fold: the fold reads the frame's counters
 }
 
