@@ -693,7 +693,13 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   // Batches: a few CTAs per frame, each looping over the frame's chunks (most
   // of a frame's chunks are empty: C5 frames fill ~45 of 256), instead of a
   // CTA per chunk.  Single frames: one CTA per chunk (streaming).
-  const int per_frame = wide ? nch : std::min(nch, kValueCtasPerFrame);
+  // (at least ~2 waves of CTAs over the whole launch: a single huge frame,
+  // e.g. a 1 cm grid, still gets a CTA per few chunks)
+  const int64_t min_per_frame = (2 * 8 * static_cast<int64_t>(ctx->n_sms) + n_frames - 1) / n_frames;
+  const int per_frame =
+      wide ? nch
+           : static_cast<int>(std::min<int64_t>(
+                 nch, std::max<int64_t>(kValueCtasPerFrame, min_per_frame)));
   cfg.gridDim = dim3(static_cast<unsigned>(n_frames * per_frame));
   const ValueFn vfn = wide ? pp::value_kernel<kCells, pp::kValueThreadsWide>
                            : pp::value_kernel<kCells, pp::kValueThreads>;

@@ -40,6 +40,14 @@ def test_c3_full_grid_bit_exact(ctx, grids_golden):
     try:
         assert lib.pp_dpps(ctx, C.byref(world), C.byref(params), C.byref(grid), kicker,
                            abi.PP_COPY_ALL, ptr) == 0, lib.pp_last_error(ctx)
+        # latency guard (north_star: well under the 16.7 ms / 60 Hz budget;
+        # measured ~1.6 ms): catches a launch-shape regression, not a benchmark
+        spans = []
+        for _ in range(3):
+            assert lib.pp_dpps(ctx, C.byref(world), C.byref(params), C.byref(grid), kicker,
+                               abi.PP_COPY_ALL, ptr) == 0, lib.pp_last_error(ctx)
+            spans.append(blk.summary.device_ms)
+        assert min(spans) < 8.0, f"C3 frame took {min(spans):.2f} ms on the device"
         fast = bytes(blk.buf)
         # the same frame with every FP32 shortcut off: byte-identical block
         assert lib.pp_ctx_set_option(ctx, abi.PP_OPT_EXACT_ONLY, 1) == 0

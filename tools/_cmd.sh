@@ -1,5 +1,2 @@
-timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/t5.log 2>&1; echo rc=$? >> gpurun_out/t5.log
-for v in rest vloop; do
-  PP_LIB_PATH=variants/libpassplan_b200_$v.so python tools/variant_bench.py 16384 3
-done > gpurun_out/variants_vloop.txt 2>&1
-PP_LIB_PATH=variants/libpassplan_b200_vloop.so python tools/variant_frame.py 1 300 >> gpurun_out/variants_vloop.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_fullsize.py tests/test_gpu_batch.py -x -q -p no:cacheprovider > gpurun_out/t6.log 2>&1; echo rc=$? >> gpurun_out/t6.log
+python tools/variant_bench.py 16384 3 >> gpurun_out/t6.log 2>&1
