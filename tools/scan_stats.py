@@ -33,6 +33,6 @@ for chip in (0, 1):
     lib.pp_debug_scan_stats(st, 1)
     pairs = st[10]
     print(f"C5 batch {n} frames chip={chip}: pairs {pairs}")
-    for i, nm in enumerate(NAMES[:15]):
+    for i, nm in enumerate(NAMES):
         print(f"  {nm:14s} {st[i]:14d}  per pair {st[i] / pairs:8.3f}")
     print(f"  SIMT lanes/step {st[13] / max(st[12], 1):.2f}")
