@@ -290,13 +290,21 @@ def run_ours(args, rank, world_size, local_rank):
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # one process per GPU; (modulo only matters for the functional gloo check,
+    # PP_BENCH_DIST_BACKEND=gloo, which may put several ranks on one device)
+    gpu = local_rank % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    backend = os.environ.get("PP_BENCH_DIST_BACKEND", "nccl")
+    coll_dev = dev if backend == "nccl" else torch.device("cpu")
     if world_size > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     lib = abi.load_library()
     ctx = C.c_void_p()
-    st = lib.pp_ctx_create(local_rank, C.byref(ctx))
+    st = lib.pp_ctx_create(gpu, C.byref(ctx))
     if st != 0:
         raise RuntimeError(f"pp_ctx_create failed ({st})")
 
@@ -325,7 +333,7 @@ def run_ours(args, rank, world_size, local_rank):
     def max_over_ranks(x):
         if world_size == 1:
             return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        t = torch.tensor([x], device=coll_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -340,7 +348,7 @@ def run_ours(args, rank, world_size, local_rank):
     barrier()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler(gpu) as clocks:
         barrier()
         t_wall0 = time.perf_counter()
         with torch.cuda.stream(stream):
@@ -364,7 +372,7 @@ def run_ours(args, rank, world_size, local_rank):
     if world_size > 1:
         rows = -(-n_total // world_size) + 1
         gather_buf = torch.zeros((rows, C.sizeof(abi.FrameSummary)), dtype=torch.uint8,
-                                 device=dev)
+                                 device=coll_dev)
         gathered = [torch.zeros_like(gather_buf) for _ in range(world_size)] if rank == 0 \
             else None
 
@@ -400,7 +408,19 @@ def run_ours(args, rank, world_size, local_rank):
         for r in range(world_size):
             a, b = shard_range(n_total, r, world_size)
             parts.append(gathered[r][:b - a].cpu().numpy())
-        gathered_ok = int(sum(p.shape[0] for p in parts)) == n_total
+        # every rank's shard is checked on rank 0's own GPU on a sample of its
+        # frames (untimed): the gathered rows must be byte-identical
+        ok = int(sum(p.shape[0] for p in parts)) == n_total
+        for r in range(world_size):
+            a, b = shard_range(n_total, r, world_size)
+            m = min(64, b - a)
+            if m <= 0:
+                continue
+            chk = (abi.FrameSummary * m)()
+            fr, _keep = synthetic.as_ctypes(synthetic.c5_frames(a, a + m))
+            check(lib.pp_dpps_frames(ctx, fr, m, C.byref(params), C.byref(grid), None, chk))
+            ok = ok and bytes(chk) == parts[r][:m].tobytes()
+        gathered_ok = ok
 
     # ---- kernel split of one step (events between the kernels, no overlap) --
     stage_ms, scan_ms, value_ms = C.c_float(), C.c_float(), C.c_float()
@@ -444,7 +464,7 @@ def run_ours(args, rank, world_size, local_rank):
                     "h2d_bytes_per_step": n_total * C.sizeof(abi.World),
                     "d2h_bytes_per_step": n_total * C.sizeof(abi.FrameSummary),
                     "path": "pp_dpps_frames (pinned host frames in, 48 B/frame results out)"
-                            + (f" + NCCL gather of all {world_size} ranks' results on rank 0"
+                            + (f" + {backend} gather of all {world_size} ranks' results on rank 0"
                                if world_size > 1 else "")},
             "roofline": {"bound": "fp32-core", "achieved": achieved, "peak": peak_tflops,
                          "unit": "TFLOP/s", "frac": achieved / peak_tflops,
