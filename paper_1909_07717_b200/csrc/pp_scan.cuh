@@ -81,6 +81,7 @@ struct CellLane {
   Traj tr;
   double ux, uy;          // unit direction
   double ax, ay, bx, by;  // first / last sample of the window (prune)
+  double s_lo, s_hi;      // ... and their distances along the ray
   double rest_x, rest_y;  // rest point
   int kb, ke;             // window [kb, ke)
   bool valid, rif;        // power exists / ball rests in the field
@@ -128,6 +129,7 @@ struct ScanSmem {
   int32_t ke[32];
   int32_t cap[2][32];  // earliest hit sample per team and cell (team cap)
   TrajF trf[32];  // FP32 trajectory per cell
+  float2 win_s[32];  // FP32 ray distances of each cell's first / last window sample
   float2 tile_uf;  // FP32 unit direction of the tile
   // per scanned robot: FP32 filter constants and the FP64 speed bound
   RobotK rk[kMaxRobots];
@@ -395,9 +397,12 @@ __device__ __forceinline__ CellLane cell_window(const FrameDev& F, const DevPara
   c.rest_x = (ox + ux * tr.d_stop).v;
   c.rest_y = (oy + uy * tr.d_stop).v;
   c.ax = c.ay = c.bx = c.by = 0.0;
+  c.s_lo = c.s_hi = 0.0;
   if (kb < ke) {
     const xd s_lo = distance_at(tr, slide, roll, xd(double(kb)) * dt);
     const xd s_hi = distance_at(tr, slide, roll, xd(double(ke - 1)) * dt);
+    c.s_lo = s_lo.v;
+    c.s_hi = s_hi.v;
     c.ax = (ox + ux * s_lo).v;
     c.ay = (oy + uy * s_lo).v;
     c.bx = (ox + ux * s_hi).v;
@@ -558,6 +563,30 @@ __device__ __forceinline__ void pair_result(const CellLane& c, const DevParams& 
   *code_out = code;
 }
 
+// Result of a finished (robot, cell) scan (dpps.cpp:177-190): a hit, capped
+// out, else the rest rule -- skipped, as (+inf, never), where a robot of the
+// same team has already hit strictly before the ball comes to rest: the
+// rest-rule time max(arrival, t_stop) >= t_stop is then later than that
+// hit, so it can neither win nor tie the team's champion (the only robot
+// whose time and id reach the outputs, dpps.cpp:192-213).  The team cap only
+// decreases, so reading it early is conservative.  cap_lane points at this
+// cell's entry of the team-cap table (cap_lane[team * 32]).
+__device__ __forceinline__ void pair_finish(const CellLane& c, const FrameDev& F,
+                                            const DevParams& P, const RobotK& rk, int ri,
+                                            int hit, bool capped, const int* cap_lane,
+                                            double* t_out, int* code_out) {
+  if (hit < 0 && !capped && c.valid && c.rif) {
+    const int team = F.scan_slot[ri] >= kTheirs ? 1 : 0;
+    const int k_team = *reinterpret_cast<const volatile int*>(cap_lane + team * 32);
+    if (k_team != 0x7fffffff && xd(double(k_team)) * xd(P.dt) < c.tr.t_stop) {
+      *t_out = CUDART_INF;
+      *code_out = -2;
+      return;
+    }
+  }
+  pair_result(c, P, robot_x(F, P, rk, ri), hit, capped, t_out, code_out);
+}
+
 // The scan's own outcome of a finished pair: a hit, capped out, or kNoHit --
 // no sample hit, the rest rule decides (resolved by rest_rule_pass once every
 // robot of the tile is done).
@@ -601,21 +630,16 @@ __device__ __forceinline__ void rest_rule_pass(const CellLane* cl, const FrameDe
 // scan_robot's prunes (intercept.cpp:89-113) in FP32 with 1e-3 m of slack --
 // the window is skipped, or the scan starts late, only where every sample
 // certainly fails the quick reject.  Exact-only mode: the window start.
-__device__ __forceinline__ int scan_start(const CellLane& c, const SampleF& S, const FrameDev& F,
-                                          int ri) {
+__device__ __forceinline__ int scan_start(const CellLane& c, const SampleF& S, float2 win_s) {
   const int kb = c.kb;
   const int ke = c.valid ? c.ke : 0;
   if (!(c.valid && kb < ke)) return ke;
   if (S.exact) return kb;
-  const int slot = F.scan_slot[ri];
-  const float rx0 = static_cast<float>(F.px[slot]), ry0 = static_cast<float>(F.py[slot]);
-  const float ax = static_cast<float>(c.ax), ay = static_cast<float>(c.ay);
-  const float abx = static_cast<float>(c.bx) - ax;
-  const float aby = static_cast<float>(c.by) - ay;
-  const float len2 = abx * abx + aby * aby;
-  float tt = len2 > 0.f ? __fdividef((rx0 - ax) * abx + (ry0 - ay) * aby, len2) : 0.f;
-  tt = fminf(fmaxf(tt, 0.f), 1.f);
-  const float ex = ax + abx * tt - rx0, ey = ay + aby * tt - ry0;
+  // segment_distance(robot, a, b) for a, b on the ray (a = ball + u s_lo,
+  // b = ball + u s_hi): the distance to the ray point at the robot's own ray
+  // coordinate s0 clamped to [s_lo, s_hi]
+  const float sc = fminf(fmaxf(S.s0, win_s.x), win_s.y);
+  const float ex = fmaf(S.uxf, sc, S.bxf), ey = fmaf(S.uyf, sc, S.byf);
   const float gap = sqrt_a(ex * ex + ey * ey) - 1e-3f - S.radf;
   if (gap > S.vbf * static_cast<float>(ke - 1) * S.dtf * 1.0001f) return ke;
   int k = kb;
@@ -640,14 +664,17 @@ __device__ __forceinline__ int scan_start(const CellLane& c, const SampleF& S, c
 // after that returns its next sample in *left_k (the CTA finishes it in
 // scan_leftovers with many lanes per cell); otherwise *left_k = -1 and the
 // result is in *t_out / *code_out.
-__device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_in, const SampleF& S,
-                                           const FrameDev& F, const DevParams& P,
+// kEager: resolve the rest rule here (throughput shape, no extra pass);
+// else leave kNoHit for rest_rule_pass (latency shapes, final team caps).
+template <bool kEager>
+__device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_in, float2 win_s,
+                                           const SampleF& S, const FrameDev& F, const DevParams& P,
                                            const RobotK& rk, int* cap,
                                            int ri, int max_steps, double* t_out,
                                            int* code_out, int* left_k) {
   const int lane = threadIdx.x & 31;
   const int ke = c.valid ? c.ke : 0;
-  int k = scan_start(c, S, F, ri);
+  int k = scan_start(c, S, win_s);
   PP_STAT(10);
   if (k >= ke) PP_STAT(11);
   const TrajF trf = trf_in;
@@ -717,7 +744,11 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
     return;
   }
   *left_k = -1;
-  pair_outcome(hit, capped, P, t_out, code_out);
+  if (kEager) {
+    pair_finish(c, F, P, rk, ri, hit, capped, cap + lane, t_out, code_out);
+  } else {
+    pair_outcome(hit, capped, P, t_out, code_out);
+  }
 }
 
 // Scan pairs left over by scan_robot: left[] holds ri << 5 | cell and
@@ -977,6 +1008,7 @@ __device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, cons
       }
       sm.ke[lane] = c.ke;
       sm.trf[lane] = TrajF(c.tr, static_cast<float>(slide.v), static_cast<float>(roll.v));
+      sm.win_s[lane] = make_float2(static_cast<float>(c.s_lo), static_cast<float>(c.s_hi));
       if (lane == 0) sm.tile_uf = make_float2(static_cast<float>(c.ux), static_cast<float>(c.uy));
       PP_CMARK_W(0);
     }
@@ -1015,7 +1047,8 @@ __device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, cons
     // first -- the longest scans, and the earliest team caps -- pulled
     // dynamically by the warps (sm.next_pair counts robots here), so the
     // warps reach the barrier together.  Every warp ranks the robots the
-    // same way (lane = robot); order does not change results.
+    // same way (lane = robot; concurrently, which measured faster than
+    // one ranking behind a barrier); order does not change results.
 #ifndef PP_SCAN_STATIC_ORDER
     constexpr bool kDyn = !kLeftovers;
 #else
@@ -1052,7 +1085,8 @@ __device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, cons
       double time;
       int code, lk;
       PP_ROBOT_START();
-      scan_robot(cl[lane], sm.trf[lane], S, F, P, rk, &sm.cap[0][0], ri, max_steps, &time,
+      scan_robot<!kLeftovers>(cl[lane], sm.trf[lane], sm.win_s[lane], S, F, P, rk, &sm.cap[0][0], ri,
+                 max_steps, &time,
                  &code, &lk);
       // an open pair: NaN time (no result is NaN) and its next sample
       sm.res_t[ri][lane] = lk < 0 ? time : CUDART_NAN;
@@ -1096,8 +1130,10 @@ __device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, cons
         __syncthreads();
       }
     }
-    rest_rule_pass(cl, F, P, sm.rk, sm.cap, sm.res_t, sm.res_k);
-    __syncthreads();
+    if (kLeftovers) {
+      rest_rule_pass(cl, F, P, sm.rk, sm.cap, sm.res_t, sm.res_k);
+      __syncthreads();
+    }
     PP_TMARK(1);
     PP_CMARK(0);
 

@@ -1,1 +1,6 @@
-PP_BENCH_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 2 --warmup 3 --frames 8192 --no-cpu --no-extras > gpurun_out/mr.json 2> gpurun_out/mr.err; echo rc=$? >> gpurun_out/mr.err
+timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/t14.log 2>&1; echo rc=$? >> gpurun_out/t14.log
+for v in mix; do
+  PP_LIB_PATH=variants/libpassplan_b200_$v.so python tools/variant_bench.py 16384 3
+  PP_LIB_PATH=variants/libpassplan_b200_$v.so python tools/variant_frame.py 1 300
+  PP_LIB_PATH=variants/libpassplan_b200_$v.so python tools/variant_frame.py 0 300
+done > gpurun_out/variants_mix.txt 2>&1
