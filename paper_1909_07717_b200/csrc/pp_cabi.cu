@@ -1443,9 +1443,9 @@ pp_status pp_score_running_points(pp_ctx* ctx, const pp_world* world, const pp_p
 // filter statistics (pp_scan.cuh g_scan_stats).
 void pp_debug_scan_stats(unsigned long long* out16, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out16, pp::g_scan_stats, 16 * sizeof(unsigned long long));
+  cudaMemcpyFromSymbol(out16, pp::g_scan_stats, 24 * sizeof(unsigned long long));
   if (reset) {
-    unsigned long long z[16] = {};
+    unsigned long long z[24] = {};
     cudaMemcpyToSymbol(pp::g_scan_stats, z, sizeof(z));
   }
 }

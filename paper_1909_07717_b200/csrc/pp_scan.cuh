@@ -414,7 +414,7 @@ __device__ __forceinline__ CellLane cell_window(const FrameDev& F, const DevPara
 // Dev statistics of the filters (variant build -DPP_SCAN_STATS only; read
 // with pp_debug_scan_stats): sample outcomes, skipped samples, warp steps.
 #ifdef PP_SCAN_STATS
-__device__ unsigned long long g_scan_stats[16];
+__device__ unsigned long long g_scan_stats[24];
 #define PP_STAT(i) atomicAdd(&g_scan_stats[i], 1ull)
 #define PP_STATN(i, n) atomicAdd(&g_scan_stats[i], static_cast<unsigned long long>(n))
 #else
@@ -681,6 +681,9 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
   int hit = -1;
   bool capped = false;
   int state = k >= ke ? 2 : 0;  // 0 scanning, 1 candidate pending, 2 finished
+#ifdef PP_SCAN_STATS
+  int n_tests = 0;
+#endif
   PP_CNT_DECL();
   // Warp-synchronous: each step every scanning lane examines one sample (or
   // certifies a run of them infeasible); lanes the FP32 bounds cannot decide
@@ -718,6 +721,9 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
     PP_STEP_PLAIN();
     if (state == 0) {
       PP_CNT(c_it);
+#ifdef PP_SCAN_STATS
+      ++n_tests;
+#endif
       int next = k;
       const int code = test_sample(rk, S, k, trf, ke, *vcap, &next);
       switch (code) {
@@ -738,6 +744,16 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
     }
   }
   PP_CNT_FLUSH();
+#ifdef PP_SCAN_STATS
+  // tests by outcome: 16/17 hit (count, tests), 18/19 capped, 20/21 window end
+  {
+    const int o = hit >= 0 ? 16 : (capped ? 18 : 20);
+    if (state == 2 && k < ke + 1 && n_tests > 0) {
+      PP_STAT(o);
+      PP_STATN(o + 1, n_tests);
+    }
+  }
+#endif
   if (state != 2) {
     PP_STAT(14);
     *left_k = k;
@@ -1064,7 +1080,9 @@ __device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, cons
         const float ex = -rk.bxf - along * u.x, ey = -rk.byf - along * u.y;
         key = ex * ex + ey * ey;
       }
-      for (int j = 0; j < 32; ++j) {
+      // (lanes >= n_scan hold the largest key: ranks of the scanned robots
+      // only count the scanned robots)
+      for (int j = 0; j < F.n_scan; ++j) {
         const float kj = __shfl_sync(0xffffffffu, key, j);
         my_rank += (kj < key || (kj == key && j < lane)) ? 1 : 0;
       }

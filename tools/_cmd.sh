@@ -1,6 +1,4 @@
-timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/t14.log 2>&1; echo rc=$? >> gpurun_out/t14.log
-for v in mix; do
+for v in o0 o1; do
   PP_LIB_PATH=variants/libpassplan_b200_$v.so python tools/variant_bench.py 16384 3
-  PP_LIB_PATH=variants/libpassplan_b200_$v.so python tools/variant_frame.py 1 300
-  PP_LIB_PATH=variants/libpassplan_b200_$v.so python tools/variant_frame.py 0 300
-done > gpurun_out/variants_mix.txt 2>&1
+done > gpurun_out/variants_order.txt 2>&1
+for v in o0s o1s; do PP_LIB_PATH=variants/libpassplan_b200_$v.so python tools/scan_stats.py 1024 | head -30; done >> gpurun_out/variants_order.txt 2>&1

@@ -13,7 +13,7 @@ from paper_1909_07717_b200 import abi, synthetic  # noqa: E402
 
 NAMES = ["tests", "end", "cap", "reach_rej", "reach_skipped", "lb_rej", "ub_hit", "cand",
          "exact", "exact_hit", "pairs", "pairs_pruned", "warp_steps", "active_lanes",
-         "to_leftovers", "-"]
+         "to_leftovers", "-", "hit_pairs", "hit_tests", "cap_pairs", "cap_tests", "end_pairs", "end_tests", "-", "-"]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 lib = abi.load_library()
 lib.pp_debug_scan_stats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
@@ -22,7 +22,7 @@ ctx = C.c_void_p()
 assert lib.pp_ctx_create(0, C.byref(ctx)) == 0
 p = abi.Params()
 lib.pp_params_default(C.byref(p))
-st = (C.c_ulonglong * 16)()
+st = (C.c_ulonglong * 24)()
 for chip in (0, 1):
     g = abi.SearchGrid(128, 64, 1.0, 6.5, 1, chip)
     fr, keep = synthetic.as_ctypes(synthetic.c5_frames(0, n))
@@ -36,3 +36,5 @@ for chip in (0, 1):
     for i, nm in enumerate(NAMES):
         print(f"  {nm:14s} {st[i]:14d}  per pair {st[i] / pairs:8.3f}")
     print(f"  SIMT lanes/step {st[13] / max(st[12], 1):.2f}")
+    for nm, a in (("hit", 16), ("capped", 18), ("end", 20)):
+        print(f"  tests per {nm} pair {st[a + 1] / max(st[a], 1):.2f}")
