@@ -964,9 +964,11 @@ pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
   HT(3);
   // (summary.device_ms is the kernels' own span, measured on the device)
   auto enqueue = [&]() -> cudaError_t {
+    // (only a graph capture records its launch: the cached graph's node
+    // updates read ctx->rec, which a plain pageable launch must not clobber)
     cudaError_t e = launch_pipeline<true>(ctx, static_cast<const pp::FrameDev*>(ctx->frame.p), 1,
                                           P, ctx->last_threads, co_run, sum_run, nullptr, fa,
-                                          &ctx->rec);
+                                          pinned ? &ctx->rec : nullptr);
     if (e == cudaSuccess && !pinned)
       e = cudaMemcpyAsync(block, dblk, sizeof(pp_dpps_summary), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && all && !direct)

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 
 #include "passplan_b200.h"
 #include <math_constants.h>
@@ -10,6 +11,25 @@
 #include "passplan/detail/pp_math.hpp"
 
 namespace pp {
+
+// Device-side bounds checks of the checked build (-DPP_CHECKED, a verification
+// variant: tools/build_variants.sh checked -DPP_CHECKED): a failed check
+// prints its site and traps, so a test run on that build fails loudly at the
+// first out-of-range index.  Compiled out of the product.
+#ifdef PP_CHECKED
+#define PP_CHECK(cond)                                                                  \
+  do {                                                                                  \
+    if (!(cond)) {                                                                      \
+      printf("PP_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__,    \
+             #cond, static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));        \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+#else
+#define PP_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
 
 constexpr int kMaxRobots = 32;  // 16 ours + 16 theirs (world.hpp:62)
 constexpr int kTheirs = 16;     // slot offset of the opponents

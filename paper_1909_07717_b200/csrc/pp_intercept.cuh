@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(1024) intercept_kernel(const FrameDev* __restr
   path_window(B, F, dt, &kb, &ke, &rif);
   for (int ri = warp; ri < F.n_scan; ri += blockDim.x >> 5) {
     const InterceptOut r = intercept_warp(B, kb, ke, rif, F, P, rk[ri], ri, dt);
+    PP_CHECK(ri < kMaxRobots);
     if (lane == 0) out[ri] = r;
   }
 }

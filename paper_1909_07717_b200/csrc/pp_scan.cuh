@@ -800,6 +800,7 @@ __device__ __forceinline__ void scan_leftovers(const CellLane* cl, const TrajF* 
       pi = nx < static_cast<unsigned>(n_left) ? static_cast<int>(nx) : -1;
       if (pi >= 0) {
         const unsigned w = left[pi];
+        PP_CHECK(pi < n_left);
         ri = static_cast<int>(w >> 5);
         cell = static_cast<int>(w & 31u);
         k = res_k[ri][cell];
@@ -943,6 +944,7 @@ __device__ __forceinline__ void tile_champions(const CellLane& c, const FrameDev
       const unsigned rank = __popc(fm & ((1u << lane) - 1u));
       // (base + rank < cap always: a frame queues at most its cells; the
       // guard keeps dirty counters from writing past the frame's region)
+      PP_CHECK(!feas || base + rank < static_cast<unsigned>(q.cap));
       if (feas && base + rank < static_cast<unsigned>(q.cap)) {
         const int64_t pos = static_cast<int64_t>(f) * q.cap + base + rank;
         q.rx[pos] = rx.v;
@@ -961,6 +963,7 @@ __device__ __forceinline__ void tile_champions(const CellLane& c, const FrameDev
           if (n_new) {
             const unsigned c0 = base / kChunk, c1 = (base + n_new - 1) / kChunk;
             const unsigned in0 = min(n_new, (c0 + 1) * kChunk - base);
+            PP_CHECK(c1 * kChunk < static_cast<unsigned>(q.cap) + kChunk);
             atomicAdd(&P.chunk_fill[c0], in0);
             if (c1 != c0) atomicAdd(&P.chunk_fill[c1], n_new - in0);
           }
@@ -970,6 +973,8 @@ __device__ __forceinline__ void tile_champions(const CellLane& c, const FrameDev
       }
       // The cell outputs last: they may go to host memory (pinned result
       // block), and the fences above need not wait for those writes.
+      PP_CHECK(!c.valid || cell < static_cast<int64_t>(P.n_kt) * P.n_dirs * P.n_pows);
+      PP_CHECK(bs_o < 16 && bs_t < 16);
       if (kCells && c.valid) {
         out.our_time[cell] = bt_o.v;
         out.opp_time[cell] = bt_t.v;
@@ -1107,6 +1112,7 @@ __device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, cons
                  max_steps, &time,
                  &code, &lk);
       // an open pair: NaN time (no result is NaN) and its next sample
+      PP_CHECK(ri >= 0 && ri < kMaxRobots);
       sm.res_t[ri][lane] = lk < 0 ? time : CUDART_NAN;
       sm.res_k[ri][lane] = lk < 0 ? code : lk;
       PP_ROBOT_END(ri);
@@ -1135,6 +1141,7 @@ __device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, cons
         }
         __syncthreads();
         const int n_left = static_cast<int>(sm.n_left);
+        PP_CHECK(n_left <= kMaxRobots * 32);
 #ifdef PP_PHASE_CLOCKS
         if (threadIdx.x == 0) sm.tph[3] = round == 0 ? n_left : sm.tph[3] + 10000;
         if (threadIdx.x == 0 && blockIdx.x < kRecCtas && round < 8) {

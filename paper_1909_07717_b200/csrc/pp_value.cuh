@@ -72,6 +72,7 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x < m) {
+    PP_CHECK(e0 + static_cast<int64_t>(threadIdx.x) < q.cap);
     const int64_t pos = static_cast<int64_t>(f) * q.cap + e0 + threadIdx.x;
     sm.q_rx[threadIdx.x] = __ldcg(&q.rx[pos]);
     sm.q_ry[threadIdx.x] = __ldcg(&q.ry[pos]);
@@ -117,7 +118,9 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
         sm.iv_y1[slot] = pi.y1.v;
         sm.iv_y2[slot] = pi.y2.v;
         sm.iv_margin[slot] = pi.margin;
-        sm.ch_iv[e][atomicAdd(&sm.ch_n[e], 1)] = static_cast<int16_t>(slot);
+        const int at = atomicAdd(&sm.ch_n[e], 1);
+        PP_CHECK(at < kMaxTeamIv);
+        sm.ch_iv[e][at] = static_cast<int16_t>(slot);
       }
     }
   }
@@ -238,6 +241,7 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
     const double sc = score_from_view(v, sm.q_rx[e], sm.q_ry[e], sm.q_ot[e], sm.q_pt[e], F, P,
                                       feat);
     const int64_t c = sm.q_cell[e];
+    PP_CHECK(c >= 0 && c < static_cast<int64_t>(P.n_kt) * P.n_dirs * P.n_pows);
     if (kCells) out.score[c] = static_cast<float>(sc);
     // (selects, not a runtime-indexed store: bs/bc stay in registers)
     const bool s1 = sm.q_slot[e] != 0;
@@ -457,6 +461,7 @@ __global__ void __launch_bounds__(kThreads, kThreads == kValueThreadsWide ? PP_V
   for (int ch = c0; ch < n_active_lb; ch += ctas_per_frame) {
     const int e0 = ch * kChunk;
     const int m = n_q - e0 < kChunk ? (n_q - e0 > 0 ? n_q - e0 : 0) : kChunk;
+    PP_CHECK(ch < chunks_per_frame && e0 < q.cap + kChunk);
     value_chunk<kCells>(sm, P, q, out, f, e0, m, base + ch);
     if (threadIdx.x == 0) {
       int n_active = n_active_lb;

@@ -67,3 +67,35 @@ def test_runmap_pinned_equals_pageable(ctx, grids_golden):
             assert bytes(arr) == page.buf.tobytes(), step
         finally:
             lib.pp_host_free(ptr)
+
+
+def test_dpps_alternating_pinned_and_pageable(ctx, grids_golden):
+    """Pageable and pinned calls interleaved on one context (the pinned call
+    replays a cached graph whose node parameters must survive the plain
+    pageable launches in between): every call returns the same block."""
+    lib = abi.load_library()
+    w, p, grid, k, _ = case_inputs(grids_golden, "f8")
+    grid.n_directions, grid.n_powers, grid.chip = 128, 64, 1
+    n = 2 * 128 * 64
+    nbytes = int(lib.pp_grid_bytes(n))
+    ptr, arr = _pinned_copy(lib, nbytes, 0)
+    off = abi.DppsSummary.device_ms.offset
+    try:
+        want = None
+        for kind in "GPGPPGGP":
+            if kind == "P":
+                arr[:] = 0
+                st = lib.pp_dpps(ctx, C.byref(w), C.byref(p), C.byref(grid), k, abi.PP_COPY_ALL,
+                                 C.c_void_p(ptr))
+                got = bytearray(arr.tobytes())
+            else:
+                page = abi.GridBlock(n)
+                st = lib.pp_dpps(ctx, C.byref(w), C.byref(p), C.byref(grid), k, abi.PP_COPY_ALL,
+                                 page.ptr())
+                got = bytearray(bytes(page.buf))
+            assert st == 0, (kind, lib.pp_last_error(ctx))
+            got[off:off + 8] = bytes(8)  # (the kernels' own time differs per call)
+            want = want or bytes(got)
+            assert bytes(got) == want, kind
+    finally:
+        lib.pp_host_free(ptr)

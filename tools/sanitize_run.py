@@ -61,7 +61,7 @@ def main():
     first = bytes(out)
     st = lib.pp_dpps_frames(ctx, arr, 64, C.byref(params), C.byref(c1), None, out)
     assert st == 0 and bytes(out) == first
-    print("c5 batch ok", sum(int(o.n_feasible) for o in out))
+    print("c5 batch ok", sum(int(o.n_feasible[0]) for o in out))
 
     pp = abi.Params.from_buffer_copy(bytes(p))
     nv = C.c_int64()
