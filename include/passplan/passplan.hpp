@@ -11,12 +11,15 @@
 // passplan_b200.h; the small host-side helpers here (geometry, tables,
 // lattices, validation, the closed-form ball model) are the same closed forms.
 //
+// The per-pair plug-in point kernels::KernelBackend (passplan/kernels/
+// kernel.hpp) has one backend, "sm100a", whose scan_first runs on the GPU;
+// run_dpps does not call through it (one call is a single (trajectory,
+// robot) pair) but reports its name in telemetry.kernel.
+//
 // Not provided (outside the accelerated path, SURVEY.md 2 out of scope): the
-// SVG renderer (svg.hpp, SvgStyle), drag_decision / DragDecision, and the
-// per-pair plug-in point kernels::KernelBackend with detail_intercept's
-// scan_window / make_kin / scan_robot (one call there is a single
-// (trajectory, robot) pair; the GPU replaces the layer above, run_dpps --
-// telemetry.kernel names the backend "sm100a").
+// SVG renderer (svg.hpp, SvgStyle), drag_decision / DragDecision, the JSON
+// serialisation of PlannerConfig (to_json_text) and the reference's CPU scan
+// backends (scalar_kernel / avx2_kernel).
 #pragma once
 
 #include <array>
@@ -30,6 +33,8 @@
 #include <string>
 #include <utility>
 #include <vector>
+
+#include "passplan/kernels/kernel.hpp"
 
 namespace passplan {
 
@@ -460,6 +465,22 @@ struct TrajectorySamples {
 // Distance along unit u from origin to the field boundary (intercept.hpp:35-37);
 // nullopt when the origin is outside the field.
 std::optional<double> ray_exit_distance(const FieldGeometry& field, Vec2 origin, Vec2 u);
+
+// The scan's internals (intercept.hpp:52-72), for callers of the plug-in point.
+namespace detail_intercept {
+struct ScanWindow {
+  int k_begin = 0;  // first sample past a chip's airborne prefix
+  int k_end = 0;    // one past the last in-field sample
+  bool rest_in_field = false;
+};
+ScanWindow scan_window(const BallTrajectory& traj, const TrajectorySamples& samples,
+                       std::optional<double> d_exit);
+kernels::RobotKin make_kin(const RobotState& robot, const MotionLimits& limits,
+                           double robot_radius);
+// scan_robot's window prune and start skip, then backend.scan_first.
+int scan_robot(const kernels::ScanBatch& batch, const kernels::RobotKin& kin,
+               const kernels::KernelBackend& backend);
+}  // namespace detail_intercept
 
 // ---- shot, free kick, possession (pass_eval.hpp) --------------------------------
 enum class ShotReason { angle_too_small, interceptable, clear };

@@ -307,6 +307,28 @@ pp_status pp_guard_points(pp_ctx* ctx, const pp_world* world, const pp_motion_li
                           double cap, int64_t n, const double* px, const double* py,
                           double* guard_pq, double* guard_time, uint8_t* ok_out);
 
+/* ---- the reference's per-pair plug-in point -----------------------------
+ * kernels::KernelBackend::scan_first (kernels/kernel.hpp:46-53): for one ray
+ * of trajectory samples and one robot, the first k in [k_begin, k_end) whose
+ * sample passes sample_feasible (kernel.hpp:33-44), else -1.  The search
+ * (pp_dpps) does not go through this interface -- one call is a single
+ * (trajectory, robot) pair -- it is here so the reference's backend registry
+ * has a B200 entry ("sm100a").  n independent pairs per call, one warp each;
+ * ts / ss are the caller's host arrays (read for [k_begin, k_end) only). */
+typedef struct pp_robot_kin { /* kernels::RobotKin, kernel.hpp:10-16 */
+  double px, py, vx, vy, accel, decel, vmax, radius, vbound;
+} pp_robot_kin;
+
+typedef struct pp_scan_batch { /* kernels::ScanBatch, kernel.hpp:20-27 */
+  const double* ts;
+  const double* ss;
+  int32_t k_begin, k_end; /* k_end exclusive */
+  double ox, oy, ux, uy;
+} pp_scan_batch;
+
+pp_status pp_scan_first(pp_ctx* ctx, int64_t n, const pp_scan_batch* batches,
+                        const pp_robot_kin* kins, int32_t* first_k);
+
 /* ---- batched frames (log replay / what-if states) ----------------------
  * Independent frames share params and grid; each gets the pp_dpps summary.
  * kicker_ids may be NULL: then the kicker is the teammate nearest the ball

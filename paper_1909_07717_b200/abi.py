@@ -358,5 +358,5 @@ EXPORTED_SYMBOLS = (
     "pp_dpps_batch", "pp_batch_upload", "pp_batch_run", "pp_batch_download", "pp_dpps_frames",
     "pp_batch_kernel_times",
     "pp_score_running_points", "pp_kick_trajectory", "pp_intercept_all", "pp_possession",
-    "pp_decide_shot", "pp_plan_free_kick", "pp_guard_points",
+    "pp_decide_shot", "pp_plan_free_kick", "pp_guard_points", "pp_scan_first",
 )

@@ -173,6 +173,40 @@ def build_ref_acceptance(force: bool = False):
     return REF_ACCEPTANCE
 
 
+REF_UNIT = os.path.join(ROOT, "tests", "cpp", "build", "ref_unit_tests")
+REF_UNIT_FILES = ("test_ball_model", "test_motion", "test_world", "test_dpps", "test_intercept",
+                  "test_pass_eval", "test_offball")
+
+
+def build_ref_unit_tests(force: bool = False):
+    """tests/cpp/build/ref_unit_tests: the reference's own unit tests
+    (proj/tests/test_*.cpp, compiled unmodified where they lie) linked against
+    the drop-in, with the test-only doctest stand-in tests/cpp/doctest_shim
+    (doctest is not vendored in the reference) and the drag_decision stub.
+    Left out: test_kernels (the reference's CPU scan backends), test_config /
+    test_outputs / test_cli (SVG style, config JSON writer, the CLI binary:
+    out of scope).  Built when the reference tree exists."""
+    srcs = [os.path.join(REF_TESTS, f + ".cpp") for f in REF_UNIT_FILES]
+    if not all(os.path.exists(x) for x in srcs):
+        return None
+    shim = os.path.join(ROOT, "tests", "cpp", "doctest_shim")
+    stub = os.path.join(ROOT, "tests", "cpp", "acceptance_stub.hpp")
+    hdrs = [os.path.join(shim, "doctest.h"), stub, DROPIN_LIB]
+    for d, _, fs in os.walk(os.path.join(ROOT, "include", "passplan")):
+        hdrs += [os.path.join(d, f) for f in fs]
+    os.makedirs(os.path.dirname(REF_UNIT), exist_ok=True)
+    if force or _stale(REF_UNIT, srcs + hdrs):
+        main_tu = os.path.join(os.path.dirname(REF_UNIT), "ref_unit_main.cpp")
+        with open(main_tu, "w") as f:
+            f.write('#define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN\n#include "doctest.h"\n')
+        data = os.path.join(ROOT, "tests", "golden", "data")
+        _run([shutil.which("g++") or "g++", "-std=c++20", "-O1", "-ffp-contract=off",
+              "-I", shim, "-I", os.path.join(ROOT, "include"), "-I", REF_TESTS,
+              "-include", stub, f'-DPASSPLAN_DATA_DIR="{data}"', main_tu, *srcs, "-o", REF_UNIT,
+              "-L", LIB_DIR, "-lpassplan", "-lpassplan_b200", f"-Wl,-rpath,{LIB_DIR}"])
+    return REF_UNIT
+
+
 def build_checkers() -> None:
     """oracle/liboracle.so always; oracle/_ref/ when the reference tree exists
     (this container).  The GPU box only uses the prebuilt files."""
@@ -192,6 +226,7 @@ def build_all(force: bool = False) -> None:
     build_csv_tool(force=force)
     build_plan_sequence(force=force)
     build_ref_acceptance(force=force)
+    build_ref_unit_tests(force=force)
 
 
 if __name__ == "__main__":

@@ -387,7 +387,7 @@ CandidateGrid run_dpps(const WorldState& world, int kicker_id, const SearchGrid&
   out.telemetry.sbip_calls = s.sbip_calls;
   out.telemetry.wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
   out.telemetry.workers = workers < 1 ? 1 : workers;
-  out.telemetry.kernel = pp_kernel_name();
+  out.telemetry.kernel = kernels::active_kernel().name;
   out.telemetry.kicker_in_possession = s.kicker_in_possession != 0;
   return out;
 }
@@ -846,6 +846,98 @@ std::optional<double> ray_exit_distance(const FieldGeometry& field, Vec2 origin,
   if (std::isnan(s)) return std::nullopt;  // origin outside the field
   return s;
 }
+
+// ---- the per-pair plug-in point (kernels/kernel.hpp) and the scan internals --------
+
+namespace kernels {
+namespace {
+
+int scan_first_sm100a(const ScanBatch& b, const RobotKin& r) {
+  pp_ctx* ctx = context();
+  const pp_scan_batch pb{b.ts, b.ss, b.k_begin, b.k_end, b.ox, b.oy, b.ux, b.uy};
+  const pp_robot_kin pk{r.px, r.py, r.vx, r.vy, r.accel, r.decel, r.vmax, r.radius, r.vbound};
+  int32_t k = -1;
+  check(pp_scan_first(ctx, 1, &pb, &pk, &k), ctx);
+  return k;
+}
+
+}  // namespace
+
+const KernelBackend& sm100a_kernel() {
+  static const KernelBackend backend{pp_kernel_name(), &scan_first_sm100a};
+  return backend;
+}
+
+const KernelBackend& active_kernel() { return sm100a_kernel(); }
+
+std::vector<const KernelBackend*> available_kernels() { return {&sm100a_kernel()}; }
+
+}  // namespace kernels
+
+namespace detail_intercept {
+
+// intercept.cpp:45-69: the in-field, landed part of the sampled trajectory.
+ScanWindow scan_window(const BallTrajectory& traj, const TrajectorySamples& samples,
+                       std::optional<double> d_exit) {
+  ScanWindow w;
+  if (!d_exit) return w;  // origin outside the field: nothing to scan
+  w.k_end = samples.count();
+  w.rest_in_field = !(*d_exit < traj.stop_distance);
+  if (!w.rest_in_field) {
+    const auto t_exit = traj.travel_time_to_distance(*d_exit);
+    const int k_last = t_exit ? static_cast<int>(std::floor(*t_exit / samples.dt + 1e-9))
+                              : samples.count() - 1;
+    w.k_end = std::min(w.k_end, k_last + 1);
+  }
+  if (traj.interceptable_from > 0.0) {
+    if (const auto t_air = traj.travel_time_to_distance(traj.interceptable_from))
+      w.k_begin = static_cast<int>(std::ceil(*t_air / samples.dt - 1e-9));
+  }
+  return w;
+}
+
+// intercept.cpp:72-85
+kernels::RobotKin make_kin(const RobotState& robot, const MotionLimits& limits,
+                           double robot_radius) {
+  kernels::RobotKin k;
+  k.px = robot.position.x;
+  k.py = robot.position.y;
+  k.vx = robot.velocity.x;
+  k.vy = robot.velocity.y;
+  k.accel = limits.max_accel;
+  k.decel = limits.max_decel;
+  k.vmax = limits.max_speed;
+  k.radius = robot_radius;
+  k.vbound = std::max(robot.velocity.norm(), limits.max_speed);
+  return k;
+}
+
+// intercept.cpp:87-115: the whole-window prune (closest point of the scanned
+// segment out of reach at the last sample time), the start skip (samples
+// before (dmin - radius - 1e-9) / vbound fail the quick reject), then the
+// backend's scan.
+int scan_robot(const kernels::ScanBatch& batch, const kernels::RobotKin& kin,
+               const kernels::KernelBackend& backend) {
+  if (batch.k_begin >= batch.k_end) return -1;
+  const double t_hi = batch.ts[batch.k_end - 1];
+  const double s_lo = batch.ss[batch.k_begin], s_hi = batch.ss[batch.k_end - 1];
+  const Vec2 a{batch.ox + batch.ux * s_lo, batch.oy + batch.uy * s_lo};
+  const Vec2 b{batch.ox + batch.ux * s_hi, batch.oy + batch.uy * s_hi};
+  const double dmin = segment_distance({kin.px, kin.py}, a, b);
+  if (dmin - kin.radius > kin.vbound * t_hi) return -1;
+  kernels::ScanBatch clipped = batch;
+  if (kin.vbound > 0.0) {
+    const double t_lo = (dmin - kin.radius - 1e-9) / kin.vbound;
+    if (t_lo > 0.0) {
+      clipped.k_begin = static_cast<int>(
+          std::lower_bound(batch.ts + batch.k_begin, batch.ts + batch.k_end, t_lo) - batch.ts);
+      if (clipped.k_begin >= clipped.k_end) return -1;
+    }
+  }
+  return backend.scan_first(clipped, kin);
+}
+
+}  // namespace detail_intercept
 
 // ---- interception, possession, shot, free kick (GPU via the C-ABI) ---------------
 

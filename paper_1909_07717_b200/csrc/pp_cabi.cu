@@ -1453,6 +1453,52 @@ void pp_debug_scan_stats(unsigned long long* out16, int reset) {
 }
 #endif
 
+pp_status pp_scan_first(pp_ctx* ctx, int64_t n, const pp_scan_batch* batches,
+                        const pp_robot_kin* kins, int32_t* first_k) {
+  if (!ctx || (n > 0 && (!batches || !kins || !first_k)) || n < 0)
+    return fail(ctx, PP_INTERNAL, "null argument");
+  ctx->err.clear();
+  if (n == 0) return PP_OK;
+  PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  std::vector<pp::ScanPair> pairs(static_cast<size_t>(n));
+  std::vector<double> samples;
+  for (int64_t i = 0; i < n; ++i) {
+    const pp_scan_batch& b = batches[i];
+    const pp_robot_kin& r = kins[i];
+    pp::ScanPair& q = pairs[static_cast<size_t>(i)];
+    q = pp::ScanPair{b.ox, b.oy, b.ux, b.uy, r.px, r.py, r.vx, r.vy, r.accel, r.decel, r.vmax,
+                     r.radius, r.vbound, static_cast<int64_t>(samples.size() / 2), b.k_begin,
+                     b.k_end};
+    if (b.k_end > b.k_begin) {
+      if (!b.ts || !b.ss) return fail(ctx, PP_INTERNAL, "null sample arrays");
+      for (int32_t k = b.k_begin; k < b.k_end; ++k) {
+        samples.push_back(b.ts[k]);
+        samples.push_back(b.ss[k]);
+      }
+    }
+  }
+  if (samples.empty()) samples.assign(2, 0.0);
+  // (samples start 16-byte aligned: they are read as double2)
+  const size_t pb = (pairs.size() * sizeof(pp::ScanPair) + 15) / 16 * 16;
+  const size_t sb = samples.size() * sizeof(double);
+  PP_CUDA_TRY(ctx, ctx->scratch_in.reserve(ctx->stream, pb + sb));
+  PP_CUDA_TRY(ctx, ctx->scratch_out.reserve(ctx->stream, static_cast<size_t>(n) * sizeof(int32_t)));
+  cudaStream_t s = ctx->stream;
+  char* din = static_cast<char*>(ctx->scratch_in.p);
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(din, pairs.data(), pairs.size() * sizeof(pp::ScanPair),
+                                   cudaMemcpyHostToDevice, s));
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(din + pb, samples.data(), sb, cudaMemcpyHostToDevice, s));
+  const int64_t threads = n * 32;
+  pp::scan_first_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
+      reinterpret_cast<const pp::ScanPair*>(din), n, reinterpret_cast<const double2*>(din + pb),
+      static_cast<int32_t*>(ctx->scratch_out.p));
+  PP_CUDA_TRY(ctx, cudaGetLastError());
+  PP_CUDA_TRY(ctx, cudaMemcpyAsync(first_k, ctx->scratch_out.p, static_cast<size_t>(n) * sizeof(int32_t),
+                                   cudaMemcpyDeviceToHost, s));
+  PP_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  return PP_OK;
+}
+
 pp_status pp_guard_points(pp_ctx* ctx, const pp_world* world, const pp_motion_limits* limits,
                           double cap, int64_t n, const double* px, const double* py,
                           double* guard_pq, double* guard_time, uint8_t* ok_out) {

@@ -53,4 +53,49 @@ __global__ void __launch_bounds__(256) score_cells_kernel(const FrameDev* __rest
   for (int k = 0; k < 5; ++k) out6[6 * q + 1 + k] = feat[k];
 }
 
+// ---------------------------------------------------------------------------
+// kernels::KernelBackend::scan_first (kernel.hpp:33-53) for n independent
+// (ray, robot) pairs: one warp per pair, 32 consecutive samples per step with
+// the reference's exact test (FP64, no FP32 filter: a plug-in call is a
+// single pair, there is nothing to amortise), the first passing sample by
+// ballot.  samples: every pair's [k_begin, k_end) (t, s) values, packed at
+// off[i].
+struct ScanPair {
+  double ox, oy, ux, uy;
+  double px, py, vx, vy, a, b, vmax, radius, vbound;
+  int64_t off;
+  int32_t k_begin, k_end;
+};
+
+__global__ void __launch_bounds__(256) scan_first_kernel(const ScanPair* __restrict__ pairs,
+                                                         int64_t n,
+                                                         const double2* __restrict__ samples,
+                                                         int32_t* __restrict__ out) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const ScanPair& q = pairs[i];
+  int first = -1;
+  for (int k0 = q.k_begin; k0 < q.k_end; k0 += 32) {
+    const int k = k0 + lane;
+    bool ok = false;
+    if (k < q.k_end) {
+      const double2 ts = samples[q.off + (k - q.k_begin)];
+      const xd t = ts.x, s = ts.y;
+      const xd qx = (xd(q.ox) + xd(q.ux) * s) - xd(q.px);
+      const xd qy = (xd(q.oy) + xd(q.uy) * s) - xd(q.py);
+      const xd d2 = qx * qx + qy * qy;
+      const xd reach = xd(q.radius) + xd(q.vbound) * t;
+      ok = !(d2 > reach * reach) &&
+           arrival_given(qx, qy, d2, q.vx, q.vy, q.a, q.b, q.vmax, q.radius) <= t;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if (m) {
+      first = k0 + __ffs(m) - 1;
+      break;
+    }
+  }
+  if (lane == 0) out[i] = first;
+}
+
 }  // namespace pp

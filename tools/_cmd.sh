@@ -1,3 +1,2 @@
-PP_LIB_PATH=variants/libpassplan_b200_checked.so timeout 1500 python -m pytest tests -m gpu -v -p no:cacheprovider > gpurun_out/checked_tests2.log 2>&1; echo rc=$? >> gpurun_out/checked_tests2.log
-PP_LIB_PATH=variants/libpassplan_b200_checked.so timeout 600 python tools/sanitize_run.py >> gpurun_out/checked_tests2.log 2>&1; echo rc=$? >> gpurun_out/checked_tests2.log
-PP_LIB_PATH=variants/libpassplan_b200_checked.so timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu --no-extras > gpurun_out/checked_bench.json 2>> gpurun_out/checked_tests2.log; echo bench rc=$? >> gpurun_out/checked_tests2.log
+DOCTEST_SKIP=drag timeout 900 tests/cpp/build/ref_unit_tests > gpurun_out/ref_unit2.log 2>&1; echo rc=$? >> gpurun_out/ref_unit2.log
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/t18.log 2>&1; echo rc=$? >> gpurun_out/t18.log
