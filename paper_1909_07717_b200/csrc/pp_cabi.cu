@@ -20,9 +20,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "passplan_b200.h"
 #include "passplan_b200_layout.h"
 #include "pp_kernels.cuh"
+
+// NVTX ranges around the C-ABI entry points (profiler ranges);
+// header-only NVTX v3, a no-op unless a profiler is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define PP_NVTX(name) const NvtxRange pp_nvtx_range_(name)
 
 namespace {
 
@@ -876,6 +888,7 @@ const char* pp_last_error(const pp_ctx* ctx) { return ctx ? ctx->err.c_str() : "
 pp_status pp_dpps(pp_ctx* ctx, const pp_world* world, const pp_params* params,
                   const pp_search_grid* grid_in, int32_t kicker_id, uint32_t copy_flags,
                   void* block) {
+  PP_NVTX("pp_dpps");
   if (!ctx || !world || !params || !block) return fail(ctx, PP_INTERNAL, "null argument");
   HT(0);
   ctx->err.clear();
@@ -1080,6 +1093,7 @@ pp_status pp_score_cells(pp_ctx* ctx, const pp_world* world, const pp_params* pa
                          const double* rx, const double* ry, const double* our_time,
                          const double* opp_time, const uint8_t* feasible, double* score_out,
                          pp_pass_features* features_out) {
+  PP_NVTX("pp_score_cells");
   if (!ctx || !world || !params) return fail(ctx, PP_INTERNAL, "null argument");
   ctx->err.clear();
   for (int64_t i = 0; i < n; ++i)
@@ -1129,6 +1143,7 @@ pp_status pp_score_cells(pp_ctx* ctx, const pp_world* world, const pp_params* pa
 pp_status pp_goal_views(pp_ctx* ctx, const pp_world* world, double robot_radius, int64_t n,
                         const double* px, const double* py, double* angle, double* window_lo,
                         double* window_hi, double* target_y) {
+  PP_NVTX("pp_goal_views");
   if (!ctx || !world) return fail(ctx, PP_INTERNAL, "null argument");
   ctx->err.clear();
   if (n == 0) return PP_OK;
@@ -1340,6 +1355,7 @@ pp_status pp_runmap_count(const pp_world* world, const pp_params* params, uint32
 
 pp_status pp_runmap(pp_ctx* ctx, const pp_world* world, const pp_params* params,
                     const pp_runmap_request* req, void* block, int64_t block_vertices) {
+  PP_NVTX("pp_runmap");
   if (!ctx || !world || !params || !req || !block) return fail(ctx, PP_INTERNAL, "null argument");
   ctx->err.clear();
   std::string why;
@@ -1407,6 +1423,7 @@ pp_status pp_score_running_points(pp_ctx* ctx, const pp_world* world, const pp_p
                                   int64_t n, const double* px, const double* py,
                                   double* score_out, pp_run_features* features_out,
                                   uint8_t* ok_out) {
+  PP_NVTX("pp_score_running_points");
   if (!ctx || !world || !params) return fail(ctx, PP_INTERNAL, "null argument");
   ctx->err.clear();
   std::string why;
@@ -1455,6 +1472,7 @@ void pp_debug_scan_stats(unsigned long long* out16, int reset) {
 
 pp_status pp_scan_first(pp_ctx* ctx, int64_t n, const pp_scan_batch* batches,
                         const pp_robot_kin* kins, int32_t* first_k) {
+  PP_NVTX("pp_scan_first");
   if (!ctx || (n > 0 && (!batches || !kins || !first_k)) || n < 0)
     return fail(ctx, PP_INTERNAL, "null argument");
   ctx->err.clear();
@@ -1502,6 +1520,7 @@ pp_status pp_scan_first(pp_ctx* ctx, int64_t n, const pp_scan_batch* batches,
 pp_status pp_guard_points(pp_ctx* ctx, const pp_world* world, const pp_motion_limits* limits,
                           double cap, int64_t n, const double* px, const double* py,
                           double* guard_pq, double* guard_time, uint8_t* ok_out) {
+  PP_NVTX("pp_guard_points");
   if (!ctx || !world || !limits) return fail(ctx, PP_INTERNAL, "null argument");
   ctx->err.clear();
   if (!(cap > 0.0) || !std::isfinite(cap))
@@ -1664,6 +1683,7 @@ extern "C" {
 
 pp_status pp_batch_upload(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
                           const int32_t* kicker_ids) {
+  PP_NVTX("pp_batch_upload");
   if (!ctx || (!frames && n_frames > 0) || n_frames < 0)
     return fail(ctx, PP_INTERNAL, "null argument");
   ctx->err.clear();
@@ -1695,6 +1715,7 @@ pp_status pp_batch_upload(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
 
 pp_status pp_batch_run(pp_ctx* ctx, const pp_params* params, const pp_search_grid* grid_in,
                        float* device_ms) {
+  PP_NVTX("pp_batch_run");
   pp::DevParams P;
   pp_status st = batch_prepare(ctx, params, grid_in, &P);
   if (st != PP_OK) return st;
@@ -1733,6 +1754,7 @@ pp_status pp_batch_run(pp_ctx* ctx, const pp_params* params, const pp_search_gri
 }
 
 pp_status pp_batch_download(pp_ctx* ctx, pp_frame_summary* out) {
+  PP_NVTX("pp_batch_download");
   if (!ctx || (!out && ctx->batch_n > 0)) return fail(ctx, PP_INTERNAL, "null argument");
   if (!ctx->batch_ran) return fail(ctx, PP_INTERNAL, "pp_batch_download before pp_batch_run");
   PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
@@ -1762,6 +1784,7 @@ pp_status pp_batch_kernel_times(pp_ctx* ctx, const pp_params* params, const pp_s
 pp_status pp_dpps_frames(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
                          const pp_params* params, const pp_search_grid* grid,
                          const int32_t* kicker_ids, pp_frame_summary* out) {
+  PP_NVTX("pp_dpps_frames");
   pp_status st = pp_batch_upload(ctx, frames, n_frames, kicker_ids);
   if (st == PP_OK) st = pp_batch_run(ctx, params, grid, nullptr);
   if (st == PP_OK) st = pp_batch_download(ctx, out);
@@ -1774,6 +1797,7 @@ pp_status pp_dpps_frames(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
 pp_status pp_dpps_batch(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
                         const pp_params* params, const pp_search_grid* grid_in,
                         const int32_t* kicker_ids, pp_dpps_summary* summaries) {
+  PP_NVTX("pp_dpps_batch");
   if (!summaries && n_frames > 0) return fail(ctx, PP_INTERNAL, "null argument");
   pp_status st = pp_batch_upload(ctx, frames, n_frames, kicker_ids);
   if (st != PP_OK) return st;
@@ -1930,6 +1954,7 @@ pp_status pp_kick_trajectory(const pp_kick* kick, const pp_ball_model* ball, pp_
 
 pp_status pp_intercept_all(pp_ctx* ctx, const pp_world* world, const pp_params* params,
                            const pp_trajectory* traj, double dt, pp_intercept* out) {
+  PP_NVTX("pp_intercept_all");
   if (!ctx || !world || !params || !traj || !out) return fail(ctx, PP_INTERNAL, "null argument");
   ctx->err.clear();
   std::string why;
@@ -1959,6 +1984,7 @@ pp_status pp_intercept_all(pp_ctx* ctx, const pp_world* world, const pp_params* 
 
 pp_status pp_possession(pp_ctx* ctx, const pp_world* world, const pp_params* params,
                         pp_possession_report* out) {
+  PP_NVTX("pp_possession");
   if (!ctx || !world || !params || !out) return fail(ctx, PP_INTERNAL, "null argument");
   const int n = world->n_ours + world->n_theirs;
   if (world->n_ours < 0 || world->n_theirs < 0 || n > 2 * PP_MAX_TEAM)
@@ -1996,6 +2022,7 @@ pp_status pp_possession(pp_ctx* ctx, const pp_world* world, const pp_params* par
 
 pp_status pp_decide_shot(pp_ctx* ctx, const pp_world* world, const pp_params* params,
                          int32_t shooter_id, pp_shot_decision* out) {
+  PP_NVTX("pp_decide_shot");
   if (!ctx || !world || !params || !out) return fail(ctx, PP_INTERNAL, "null argument");
   ctx->err.clear();
   std::string why;
@@ -2032,6 +2059,7 @@ pp_status pp_decide_shot(pp_ctx* ctx, const pp_world* world, const pp_params* pa
 pp_status pp_plan_free_kick(pp_ctx* ctx, const pp_world* world, const pp_params* params,
                             int32_t kicker_id, const pp_candidate* target,
                             pp_free_kick_plan* out) {
+  PP_NVTX("pp_plan_free_kick");
   if (!ctx || !world || !params || !target || !out)
     return fail(ctx, PP_INTERNAL, "null argument");
   ctx->err.clear();
