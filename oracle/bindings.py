@@ -67,6 +67,8 @@ def ref():
                                        C.c_char_p, C.c_size_t]
         lib.ref_intercept_all.argtypes = [W, Pm, C.POINTER(abi.Kick), C.c_double,
                                           C.POINTER(abi.Intercept), C.c_char_p, C.c_size_t]
+        lib.ref_scan_first.argtypes = [C.c_int64, C.POINTER(abi.ScanBatch),
+                                       C.POINTER(abi.RobotKin), C.POINTER(C.c_int32)]
         lib.ref_csv_roundtrip.argtypes = [C.c_int32, C.c_char_p, C.c_char_p, C.c_size_t]
         lib.ref_csv_roundtrip.restype = C.c_int64
         lib.ref_guard_points.argtypes = [W, C.POINTER(abi.MotionLimits), C.c_double, C.c_int64,

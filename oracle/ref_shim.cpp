@@ -696,6 +696,35 @@ int64_t ref_csv_roundtrip(int32_t kind, const char* text, char* buf, size_t len)
   return put_text(out, buf, len);
 }
 
+// kernels::scalar_kernel().scan_first of the reference for n (ray, robot)
+// pairs (kernel.hpp:46-53); ts/ss per pair from the caller's arrays.
+int ref_scan_first(int64_t n, const pp_scan_batch* batches, const pp_robot_kin* kins,
+                   int32_t* out) {
+  for (int64_t i = 0; i < n; ++i) {
+    kernels::ScanBatch b;
+    b.ts = batches[i].ts;
+    b.ss = batches[i].ss;
+    b.k_begin = batches[i].k_begin;
+    b.k_end = batches[i].k_end;
+    b.ox = batches[i].ox;
+    b.oy = batches[i].oy;
+    b.ux = batches[i].ux;
+    b.uy = batches[i].uy;
+    kernels::RobotKin r;
+    r.px = kins[i].px;
+    r.py = kins[i].py;
+    r.vx = kins[i].vx;
+    r.vy = kins[i].vy;
+    r.accel = kins[i].accel;
+    r.decel = kins[i].decel;
+    r.vmax = kins[i].vmax;
+    r.radius = kins[i].radius;
+    r.vbound = kins[i].vbound;
+    out[i] = kernels::scalar_kernel().scan_first(b, r);
+  }
+  return 0;
+}
+
 // `passplan plan --out` CSV of one frame (passplan_main.cpp:89, csv.cpp:85-114).
 // Returns the text length (buf gets a NUL-terminated copy, truncated to len).
 int64_t ref_grid_csv(const pp_world* world, const pp_params* params, int32_t kicker_id,

@@ -107,6 +107,16 @@ class FrameSummary(C.Structure):  # pp_frame_summary (48 B per frame)
     _fields_ = [("best_score", _D * 3), ("best_cell", _I * 3), ("n_feasible", _I * 3)]
 
 
+class RobotKin(C.Structure):  # pp_robot_kin (kernels::RobotKin)
+    _fields_ = [(n, _D) for n in ("px", "py", "vx", "vy", "accel", "decel", "vmax", "radius",
+                                  "vbound")]
+
+
+class ScanBatch(C.Structure):  # pp_scan_batch (kernels::ScanBatch)
+    _fields_ = [("ts", C.POINTER(_D)), ("ss", C.POINTER(_D)), ("k_begin", _I), ("k_end", _I),
+                ("ox", _D), ("oy", _D), ("ux", _D), ("uy", _D)]
+
+
 class RunFeatures(C.Structure):
     _fields_ = [(n, _D) for n in ("dist_to_goal", "dist_to_ball", "angle_to_goal", "guard_time",
                                   "defense_exposure")]
@@ -305,6 +315,8 @@ def _declare(lib):
     lib.pp_guard_points.argtypes = [vp, _P(World), _P(MotionLimits), C.c_double, C.c_int64, dp,
                                     dp, dp, dp, _P(C.c_uint8)]
     lib.pp_guard_points.restype = C.c_int
+    lib.pp_scan_first.argtypes = [vp, C.c_int64, _P(ScanBatch), _P(RobotKin), _P(C.c_int32)]
+    lib.pp_scan_first.restype = C.c_int
     lib.pp_dpps_batch.argtypes = [vp, _P(World), C.c_int64, _P(Params), _P(SearchGrid),
                                   _P(C.c_int32), _P(DppsSummary)]
     lib.pp_batch_upload.argtypes = [vp, _P(World), C.c_int64, _P(C.c_int32)]

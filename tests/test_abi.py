@@ -46,7 +46,8 @@ STRUCTS = {"pp_world": abi.World, "pp_params": abi.Params, "pp_search_grid": abi
            "pp_dpps_summary": abi.DppsSummary, "pp_runmap_summary": abi.RunmapSummary,
            "pp_runmap_request": abi.RunmapRequest, "pp_pass_features": abi.PassFeatures,
            "pp_robot": abi.Robot, "pp_thresholds": abi.Thresholds,
-           "pp_frame_summary": abi.FrameSummary}
+           "pp_frame_summary": abi.FrameSummary, "pp_robot_kin": abi.RobotKin,
+           "pp_scan_batch": abi.ScanBatch}
 
 
 def test_struct_layouts_match_header(tmp_path):
