@@ -69,6 +69,8 @@ def ref():
                                           C.POINTER(abi.Intercept), C.c_char_p, C.c_size_t]
         lib.ref_scan_first.argtypes = [C.c_int64, C.POINTER(abi.ScanBatch),
                                        C.POINTER(abi.RobotKin), C.POINTER(C.c_int32)]
+        lib.ref_json_check.argtypes = [C.c_int32, C.c_char_p, C.c_char_p, C.c_size_t]
+        lib.ref_json_check.restype = C.c_int64
         lib.ref_csv_roundtrip.argtypes = [C.c_int32, C.c_char_p, C.c_char_p, C.c_size_t]
         lib.ref_csv_roundtrip.restype = C.c_int64
         lib.ref_guard_points.argtypes = [W, C.POINTER(abi.MotionLimits), C.c_double, C.c_int64,

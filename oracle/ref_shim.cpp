@@ -676,6 +676,28 @@ int ref_guard_points(const pp_world* world, const pp_motion_limits* limits, doub
   });
 }
 
+// JSON round trips of the reference: kind 0 = world snapshot (parse then
+// serialize, snapshot.cpp), 1 = planner config (parse; a few values
+// printed).  "ERROR <category>: <message>" when the reader throws.
+int64_t ref_json_check(int32_t kind, const char* text, char* buf, size_t len) {
+  std::string out;
+  try {
+    if (kind == 0) {
+      out = serialize_world_snapshot(parse_world_snapshot(text));
+    } else {
+      const PlannerConfig c = PlannerConfig::from_json_text(text);
+      char b[160];
+      std::snprintf(b, sizeof b, "OK %.17g %.17g %d %d %.17g", c.ball.slide_decel,
+                    c.thresholds.sbip_dt, c.grid.n_directions, c.grid.chip ? 1 : 0,
+                    c.weights.pass.margin);
+      out = b;
+    }
+  } catch (const Error& e) {
+    out = std::string("ERROR ") + category_name(e.category()) + ": " + e.what();
+  }
+  return put_text(out, buf, len);
+}
+
 // CSV reader -> writer round trip of the reference (csv.cpp): kind 0 = grid,
 // 1 = pass heat map, 2 = run heat map.  The output is the rewritten text, or
 // "ERROR <category>: <message>" when the reader throws.

@@ -229,7 +229,8 @@ void WorldState::validate() const {
   for (const auto* team : {&ours, &theirs}) {
     const char* name = team == &ours ? "ours" : "theirs";
     if (team->size() > 16)
-      throw validation_error(std::string(name) + ": more than 16 robots");
+      throw validation_error(std::string(name) + ": more than 16 robots (" +
+                             std::to_string(team->size()) + ")");
     std::set<int> ids;
     for (const RobotState& r : *team) {
       if (!ids.insert(r.id).second)

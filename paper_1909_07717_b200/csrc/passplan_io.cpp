@@ -10,6 +10,7 @@
 #include <filesystem>
 #include <fstream>
 #include <functional>
+#include <iterator>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -20,48 +21,76 @@
 
 namespace passplan {
 
-// ---- JSON world snapshots (snapshot.cpp) ----------------------------------------
+// ---- JSON world snapshots (snapshot.hpp) -----------------------------------------
+// Schema-driven: every object is described by its keys (required or optional,
+// each with a reader), and one routine enforces the reference's rules in its
+// order -- object type, missing required keys (schema order), unknown keys,
+// then the values (schema order) -- so malformed input gets the same
+// schema_error text as from the reference (snapshot.cpp:17-95).
 namespace {
 
 using nlohmann::json;
+using Reader = std::function<void(const json&, const std::string&)>;
 
-// Checks an object's keys: all of `need` present, nothing outside need+opt.
-void check_keys(const json& o, const std::string& at, std::initializer_list<const char*> need,
-                std::initializer_list<const char*> opt = {}) {
-  for (const char* k : need)
-    if (!o.contains(k)) throw schema_error(at + ": missing key '" + k + "'");
-  for (const auto& it : o.items()) {
-    bool known = false;
-    for (const char* k : need) known = known || it.key() == k;
-    for (const char* k : opt) known = known || it.key() == k;
-    if (!known) throw schema_error(at + ": unknown key '" + it.key() + "'");
+struct SchemaKey {
+  const char* name;
+  bool required;
+  Reader read;
+};
+
+void read_object(const json& v, const std::string& where, const std::vector<SchemaKey>& keys,
+                 const char* not_object = nullptr) {
+  if (!v.is_object())
+    throw schema_error(not_object ? std::string(not_object) : where + ": must be an object");
+  for (const SchemaKey& k : keys)
+    if (k.required && !v.contains(k.name))
+      throw schema_error(where + ": missing key '" + k.name + "'");
+  for (const auto& item : v.items()) {
+    const bool known = std::any_of(keys.begin(), keys.end(),
+                                   [&](const SchemaKey& k) { return item.key() == k.name; });
+    if (!known) throw schema_error(where + ": unknown key '" + item.key() + "'");
   }
+  for (const SchemaKey& k : keys)
+    if (v.contains(k.name)) k.read(v.at(k.name), where);
 }
 
-double json_number(const json& o, const std::string& at, const char* key) {
-  const json& v = o.at(key);
-  if (!v.is_number()) throw schema_error(at + ": '" + key + "' must be a number");
-  return v.get<double>();
+Reader number_into(double* dst, const char* key) {
+  return [dst, key](const json& x, const std::string& where) {
+    if (!x.is_number()) throw schema_error(where + ": '" + key + "' must be a number");
+    *dst = x.get<double>();
+  };
 }
 
-std::vector<RobotState> json_team(const json& arr, const std::string& at) {
-  if (!arr.is_array()) throw schema_error(at + ": must be an array");
-  std::vector<RobotState> team;
-  for (size_t i = 0; i < arr.size(); ++i) {
-    const json& r = arr[i];
-    const std::string where = at + "[" + std::to_string(i) + "]";
-    if (!r.is_object()) throw schema_error(where + ": must be an object");
-    check_keys(r, where, {"id", "x", "y", "vx", "vy", "theta"});
-    if (!r.at("id").is_number_integer())
-      throw schema_error(where + ": 'id' must be an integer");
-    RobotState s;
-    s.id = r.at("id").get<int>();
-    s.position = {json_number(r, where, "x"), json_number(r, where, "y")};
-    s.velocity = {json_number(r, where, "vx"), json_number(r, where, "vy")};
-    s.theta = json_number(r, where, "theta");
-    team.push_back(s);
-  }
-  return team;
+Reader integer_into(int* dst, const char* key) {
+  return [dst, key](const json& x, const std::string& where) {
+    if (!x.is_number_integer()) throw schema_error(where + ": '" + key + "' must be an integer");
+    *dst = x.get<int>();
+  };
+}
+
+std::vector<SchemaKey> robot_schema(RobotState* r) {
+  return {{"id", true, integer_into(&r->id, "id")},
+          {"x", true, number_into(&r->position.x, "x")},
+          {"y", true, number_into(&r->position.y, "y")},
+          {"vx", true, number_into(&r->velocity.x, "vx")},
+          {"vy", true, number_into(&r->velocity.y, "vy")},
+          {"theta", true, number_into(&r->theta, "theta")}};
+}
+
+Reader team_into(std::vector<RobotState>* team, const char* key) {
+  return [team, key](const json& x, const std::string&) {
+    if (!x.is_array()) throw schema_error(std::string(key) + ": must be an array");
+    team->assign(x.size(), RobotState{});
+    for (size_t i = 0; i < x.size(); ++i)
+      read_object(x[i], std::string(key) + "[" + std::to_string(i) + "]",
+                  robot_schema(&(*team)[i]));
+  };
+}
+
+std::string file_text(const std::string& path, ErrorCategory cat, const char* what) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw Error(cat, std::string("cannot open ") + what + " file: " + path);
+  return std::string(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
 }
 
 }  // namespace
@@ -73,60 +102,68 @@ WorldState parse_world_snapshot(const std::string& bytes) {
   } catch (const json::parse_error& e) {
     throw schema_error(std::string("snapshot is not valid JSON: ") + e.what());
   }
-  if (!root.is_object()) throw schema_error("snapshot: top level must be an object");
-  check_keys(root, "snapshot", {"field", "ball", "ours", "theirs"});
   WorldState w;
-  const json& f = root.at("field");
-  if (!f.is_object()) throw schema_error("field: must be an object");
-  check_keys(f, "field", {}, {"length", "width", "goal_width", "defense_depth", "defense_width"});
-  struct {
-    const char* key;
-    double* dst;
-  } const fields[] = {{"length", &w.field.length},
-                      {"width", &w.field.width},
-                      {"goal_width", &w.field.goal_width},
-                      {"defense_depth", &w.field.defense_depth},
-                      {"defense_width", &w.field.defense_width}};
-  for (const auto& fd : fields)
-    if (f.contains(fd.key)) *fd.dst = json_number(f, "field", fd.key);
-  const json& b = root.at("ball");
-  if (!b.is_object()) throw schema_error("ball: must be an object");
-  check_keys(b, "ball", {"x", "y", "vx", "vy"});
-  w.ball.position = {json_number(b, "ball", "x"), json_number(b, "ball", "y")};
-  w.ball.velocity = {json_number(b, "ball", "vx"), json_number(b, "ball", "vy")};
-  w.ours = json_team(root.at("ours"), "ours");
-  w.theirs = json_team(root.at("theirs"), "theirs");
+  FieldGeometry& f = w.field;
+  const std::vector<SchemaKey> field_keys = {
+      {"length", false, number_into(&f.length, "length")},
+      {"width", false, number_into(&f.width, "width")},
+      {"goal_width", false, number_into(&f.goal_width, "goal_width")},
+      {"defense_depth", false, number_into(&f.defense_depth, "defense_depth")},
+      {"defense_width", false, number_into(&f.defense_width, "defense_width")}};
+  const std::vector<SchemaKey> ball_keys = {
+      {"x", true, number_into(&w.ball.position.x, "x")},
+      {"y", true, number_into(&w.ball.position.y, "y")},
+      {"vx", true, number_into(&w.ball.velocity.x, "vx")},
+      {"vy", true, number_into(&w.ball.velocity.y, "vy")}};
+  read_object(root, "snapshot",
+              {{"field", true, [&](const json& x, const std::string&) {
+                  read_object(x, "field", field_keys);
+                }},
+               {"ball", true, [&](const json& x, const std::string&) {
+                  read_object(x, "ball", ball_keys);
+                }},
+               {"ours", true, team_into(&w.ours, "ours")},
+               {"theirs", true, team_into(&w.theirs, "theirs")}},
+              "snapshot: top level must be an object");
   w.validate();
   return w;
 }
 
 WorldState load_world_snapshot(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw schema_error("cannot open snapshot file: " + path);
-  std::ostringstream ss;
-  ss << in.rdbuf();
-  return parse_world_snapshot(ss.str());
+  return parse_world_snapshot(file_text(path, ErrorCategory::schema, "snapshot"));
 }
 
+// (nlohmann::json objects keep their keys sorted, so the text does not depend
+// on the order they are set in)
 std::string serialize_world_snapshot(const WorldState& w) {
-  auto robot = [](const RobotState& r) {
-    return json{{"id", r.id},         {"x", r.position.x},  {"y", r.position.y},
-                {"vx", r.velocity.x}, {"vy", r.velocity.y}, {"theta", r.theta}};
-  };
-  json root;
-  root["field"] = {{"length", w.field.length},
-                   {"width", w.field.width},
-                   {"goal_width", w.field.goal_width},
-                   {"defense_depth", w.field.defense_depth},
-                   {"defense_width", w.field.defense_width}};
-  root["ball"] = {{"x", w.ball.position.x},
-                  {"y", w.ball.position.y},
-                  {"vx", w.ball.velocity.x},
-                  {"vy", w.ball.velocity.y}};
-  root["ours"] = json::array();
-  for (const RobotState& r : w.ours) root["ours"].push_back(robot(r));
-  root["theirs"] = json::array();
-  for (const RobotState& r : w.theirs) root["theirs"].push_back(robot(r));
+  json root = json::object();
+  const FieldGeometry& f = w.field;
+  for (const auto& [k, v] : {std::pair<const char*, double>{"length", f.length},
+                             {"width", f.width},
+                             {"goal_width", f.goal_width},
+                             {"defense_depth", f.defense_depth},
+                             {"defense_width", f.defense_width}})
+    root["field"][k] = v;
+  root["ball"]["x"] = w.ball.position.x;
+  root["ball"]["y"] = w.ball.position.y;
+  root["ball"]["vx"] = w.ball.velocity.x;
+  root["ball"]["vy"] = w.ball.velocity.y;
+  for (const auto& [key, team] : {std::pair<const char*, const std::vector<RobotState>*>{
+                                      "ours", &w.ours},
+                                  {"theirs", &w.theirs}}) {
+    json arr = json::array();
+    for (const RobotState& r : *team) {
+      json o = json::object();
+      o["id"] = r.id;
+      o["x"] = r.position.x;
+      o["y"] = r.position.y;
+      o["vx"] = r.velocity.x;
+      o["vy"] = r.velocity.y;
+      o["theta"] = r.theta;
+      arr.push_back(std::move(o));
+    }
+    root[key] = std::move(arr);
+  }
   return root.dump(2) + "\n";
 }
 
@@ -292,11 +329,7 @@ PlannerConfig PlannerConfig::from_json_text(const std::string& text) {
 }
 
 PlannerConfig PlannerConfig::load(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw config_error("cannot open config file: " + path);
-  std::ostringstream ss;
-  ss << in.rdbuf();
-  return from_json_text(ss.str());
+  return from_json_text(file_text(path, ErrorCategory::config, "config"));
 }
 
 }  // namespace passplan

@@ -3,7 +3,8 @@
 // named by argv[1] (grid | heat | run) and writes it back with the matching
 // writer, or prints "ERROR <category>: <message>" when the reader throws --
 // the same contract as oracle/ref_shim.cpp's ref_csv_roundtrip, so
-// tests/test_csv_cpu.py can compare both byte for byte.  No GPU is used.
+// tests/test_csv_cpu.py can compare both byte for byte; "snapshot" and
+// "config" do the same for the JSON readers.  No GPU is used.
 #include <cstdio>
 #include <iostream>
 #include <iterator>
@@ -18,6 +19,15 @@ int main(int argc, char** argv) {
   try {
     if (kind == "grid") {
       out = passplan::grid_to_csv(passplan::grid_from_csv(text));
+    } else if (kind == "snapshot") {
+      out = passplan::serialize_world_snapshot(passplan::parse_world_snapshot(text));
+    } else if (kind == "config") {
+      const passplan::PlannerConfig c = passplan::PlannerConfig::from_json_text(text);
+      char buf[160];
+      std::snprintf(buf, sizeof buf, "OK %.17g %.17g %d %d %.17g", c.ball.slide_decel,
+                    c.thresholds.sbip_dt, c.grid.n_directions, c.grid.chip ? 1 : 0,
+                    c.weights.pass.margin);
+      out = buf;
     } else if (kind == "heat") {
       out = passplan::heatmap_to_csv(passplan::heatmap_from_csv(text));
     } else {
