@@ -371,19 +371,32 @@ CandidateGrid run_dpps(const WorldState& world, int kicker_id, const SearchGrid&
     tl.pow_hi = grid.power_max;
   }
   out.powers = tl.pows;
-  out.cells.resize(static_cast<size_t>(n));
+  // (cell order: kick slot, direction, power -- nested loops, no per-cell
+  // index arithmetic; each cell written once)
+  out.cells.reserve(static_cast<size_t>(n));
   const int nd = grid.n_directions, np = grid.n_powers;
-  for (int64_t i = 0; i < n; ++i) {
-    PassCandidate& c = out.cells[static_cast<size_t>(i)];
-    c.kick_type = out.kick_types[static_cast<size_t>(i / (int64_t(nd) * np))];
-    c.dir_index = static_cast<int>((i / np) % nd);
-    c.power_index = static_cast<int>(i % np);
-    c.our_id = v.our_slot[i] >= 0 ? s.ours_ids[v.our_slot[i]] : -1;
-    c.opp_id = v.opp_slot[i] >= 0 ? s.theirs_ids[v.opp_slot[i]] : -1;
-    c.our_time = v.our_time[i];
-    c.opp_time = v.opp_time[i];
-    if (c.our_time < kNever) c.receive_point = {v.rx[i], v.ry[i]};
-    c.feasible = v.feasible[i] != 0;
+  int ours_ids[PP_MAX_TEAM + 1], theirs_ids[PP_MAX_TEAM + 1];  // slot + 1 -> id (-1 = none)
+  ours_ids[0] = theirs_ids[0] = -1;
+  for (int k = 0; k < PP_MAX_TEAM; ++k) {
+    ours_ids[k + 1] = s.ours_ids[k];
+    theirs_ids[k + 1] = s.theirs_ids[k];
+  }
+  int64_t i = 0;
+  for (const KickType kt : out.kick_types) {
+    for (int d = 0; d < nd; ++d) {
+      for (int pw = 0; pw < np; ++pw, ++i) {
+        PassCandidate& c = out.cells.emplace_back();
+        c.kick_type = kt;
+        c.dir_index = d;
+        c.power_index = pw;
+        c.our_id = ours_ids[v.our_slot[i] + 1];
+        c.opp_id = theirs_ids[v.opp_slot[i] + 1];
+        c.our_time = v.our_time[i];
+        c.opp_time = v.opp_time[i];
+        if (c.our_time < kNever) c.receive_point = {v.rx[i], v.ry[i]};
+        c.feasible = v.feasible[i] != 0;
+      }
+    }
   }
   out.telemetry.sbip_calls = s.sbip_calls;
   out.telemetry.wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
@@ -450,15 +463,19 @@ bool cached_best_pass(const CandidateGrid& g, const WorldState& world, const Pla
   pp_grid_view v;
   pp_grid_view_of(tl.dpps_block, tl.dpps_cells, &v);
   const int nd = g.grid.n_directions, np = g.grid.n_powers;
-  for (int64_t i = 0; i < tl.dpps_cells; ++i) {
-    const PassCandidate& c = g.cells[static_cast<size_t>(i)];
-    if (c.feasible != (v.feasible[i] != 0)) return false;
-    if (!c.feasible) continue;
-    if (c.kick_type != g.kick_types[static_cast<size_t>(i / (int64_t(nd) * np))] ||
-        c.dir_index != static_cast<int>((i / np) % nd) || c.power_index != static_cast<int>(i % np) ||
-        c.our_time != v.our_time[i] || c.opp_time != v.opp_time[i] ||
-        c.receive_point.x != v.rx[i] || c.receive_point.y != v.ry[i])
-      return false;
+  int64_t i = 0;
+  for (const KickType kt : g.kick_types) {
+    for (int d = 0; d < nd; ++d) {
+      for (int pw = 0; pw < np; ++pw, ++i) {
+        const PassCandidate& c = g.cells[static_cast<size_t>(i)];
+        if (c.feasible != (v.feasible[i] != 0)) return false;
+        if (c.feasible &&
+            (c.kick_type != kt || c.dir_index != d || c.power_index != pw ||
+             c.our_time != v.our_time[i] || c.opp_time != v.opp_time[i] ||
+             c.receive_point.x != v.rx[i] || c.receive_point.y != v.ry[i]))
+          return false;
+      }
+    }
   }
   const pp_dpps_summary& s = *v.summary;
   const int which = !only ? 0 : (*only == KickType::flat ? 1 : 2);
