@@ -53,6 +53,10 @@ struct FrameCounters {
   unsigned tiles_done;  // scan tiles whose queue entries are written (streaming value)
   unsigned value_out;   // streaming: value CTAs of the frame that have left
   unsigned long long t0_inv;  // ~(earliest scan CTA start, globaltimer ns); 0 = none
+  // batches: per kick slot, the largest lower bound of a queued cell's score
+  // (score_key; 0 = none) -- cells whose upper bound is below it cannot be
+  // the slot's best_pass and skip the value function (value_chunk)
+  unsigned long long lb_key[2];
 };
 
 // Streaming waits give up after this many polls (~4 s): the CTA leaves

@@ -34,6 +34,7 @@ struct ValueSmem {
   int32_t w_idx[kMaxWarps][2];
   unsigned last;
   int n_act;  // streaming: queue size seen at start (-1 full chunk) / final chunk count
+  int n_keep;  // batch pruning: cells of the chunk left after the score bounds
 };
 
 // Warp partials of a frame fold (last chunk done).
@@ -64,10 +65,14 @@ __device__ __forceinline__ void value_heights(ValueSmem& sm, const DevParams& P)
 // then the chunk's argmax per kick slot and a last-chunk-done reduction.
 // One value chunk: queue entries [e0, e0 + m) of frame f (sm.frame loaded).
 // Thread 0 writes the chunk's Partial to *dst.
+// lb0/lb1 (batches, !kCells): the frame's score lower-bound keys per kick
+// slot; a cell whose score upper bound is below its slot's key is dropped
+// before the goal view (it cannot be best_pass), 0 = keep every cell.
 template <bool kCells>
 __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, const CellQueue& q,
                                             const CellOut& out, int f, int e0, int m,
-                                            Partial* dst) {
+                                            Partial* dst, unsigned long long lb0 = 0ull,
+                                            unsigned long long lb1 = 0ull) {
   PP_CLOCK_INIT();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -88,6 +93,43 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
   }
   if (threadIdx.x == 0) sm.iv_n = 0;
   __syncthreads();
+  if (!kCells && (lb0 | lb1)) {
+    // Batch pruning (warp 0, lane = queued cell; m <= 32): keep the cells
+    // whose score upper bound reaches their slot's best lower bound,
+    // compacted in queue order.
+    if (warp == 0) {
+      const int e = lane;
+      double rx = 0.0, ry = 0.0, ot = 0.0, pt = 0.0;
+      int32_t cell = 0;
+      int8_t slot = 0;
+      bool keep = false;
+      if (e < m) {
+        rx = sm.q_rx[e];
+        ry = sm.q_ry[e];
+        ot = sm.q_ot[e];
+        pt = sm.q_pt[e];
+        cell = sm.q_cell[e];
+        slot = sm.q_slot[e];
+        double lo, hi;
+        score_bounds(rx, ry, ot, pt, sm.frame, P, &lo, &hi);
+        keep = score_key(hi) >= (slot ? lb1 : lb0);
+      }
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      __syncwarp();
+      if (keep) {
+        const int at = __popc(km & ((1u << lane) - 1u));
+        sm.q_rx[at] = rx;
+        sm.q_ry[at] = ry;
+        sm.q_ot[at] = ot;
+        sm.q_pt[at] = pt;
+        sm.q_cell[at] = cell;
+        sm.q_slot[at] = slot;
+      }
+      if (lane == 0) sm.n_keep = __popc(km);
+    }
+    __syncthreads();
+    m = sm.n_keep;
+  }
   const FrameDev& F = sm.frame;
   const int nt = F.n_theirs;
   const xd radius = P.radius;
@@ -288,6 +330,41 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
   PP_FLUSH(9);
 }
 
+// Batches, between scan and value: per frame (one warp), the largest lower
+// bound of a queued cell's score per kick slot (score_bounds), into
+// FrameCounters::lb_key -- value_chunk then drops every cell whose upper
+// bound is below its slot's key before the goal view (it cannot be the
+// slot's best_pass).  The queue is complete: this grid runs after the scan.
+__global__ void __launch_bounds__(256) score_lb_kernel(const FrameDev* __restrict__ frames,
+                                                       DevParams P, CellQueue q,
+                                                       FrameCounters* __restrict__ fc,
+                                                       int64_t n_frames) {
+  const int64_t f = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  // (the value grid, launched programmatically after this one, waits for it)
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (f >= n_frames) return;
+  const int n = static_cast<int>(fc[f].q_count);
+  FrameDev F;  // only the field sizes are read
+  F.L = frames[f].L;
+  F.gw = frames[f].gw;
+  unsigned long long best[2] = {0ull, 0ull};
+  for (int e = lane; e < n; e += 32) {
+    const int64_t pos = f * q.cap + e;
+    double lo;
+    score_bounds<true>(q.rx[pos], q.ry[pos], q.ot[pos], q.pt[pos], F, P, &lo, nullptr);
+    const unsigned long long k = score_key(lo);
+    const int s = q.slot[pos];
+    best[s] = k > best[s] ? k : best[s];
+  }
+  for (int s = 0; s < 2; ++s) {
+    const unsigned hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(best[s] >> 32));
+    const unsigned lo = __reduce_max_sync(
+        0xffffffffu, static_cast<unsigned>(best[s] >> 32) == hi ? static_cast<unsigned>(best[s]) : 0u);
+    if (lane == 0) fc[f].lb_key[s] = (static_cast<unsigned long long>(hi) << 32) | lo;
+  }
+}
+
 // Fold the n chunk partials of frame f into its summary (all threads of the
 // CTA).  `better` is a strict total order on (score desc, cell asc), so the
 // fold order cannot change the winner.  Resets the frame's counters.
@@ -361,6 +438,8 @@ __device__ __forceinline__ void fold_frame(FoldSmem& fs, const Partial* base, in
     fcf->n_feas[0] = 0;
     fcf->n_feas[1] = 0;
     fcf->chunks_done = 0;
+    fcf->lb_key[0] = 0ull;
+    fcf->lb_key[1] = 0ull;
   }
 }
 
@@ -415,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, kThreads == kValueThreadsWide ? PP_V
     }
   };
   int n_q;
+  unsigned long long lb_key0 = 0ull, lb_key1 = 0ull;  // batch pruning bounds
   if (stream) {
     // Scan -> value streaming (single frame): start as soon as this chunk's
     // entries are written, or once every tile is done (the last, partial
@@ -445,6 +525,10 @@ __global__ void __launch_bounds__(kThreads, kThreads == kValueThreadsWide ? PP_V
   } else {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // scan grid done and visible
     n_q = static_cast<int>(fc[f].q_count);
+    if (!kCells) {
+      lb_key0 = fc[f].lb_key[0];
+      lb_key1 = fc[f].lb_key[1];
+    }
   }
   const int n_active_lb = n_q > 0 ? (n_q + kChunk - 1) / kChunk : 1;
   if (c0 >= n_active_lb) {
@@ -462,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, kThreads == kValueThreadsWide ? PP_V
     const int e0 = ch * kChunk;
     const int m = n_q - e0 < kChunk ? (n_q - e0 > 0 ? n_q - e0 : 0) : kChunk;
     PP_CHECK(ch < chunks_per_frame && e0 < q.cap + kChunk);
-    value_chunk<kCells>(sm, P, q, out, f, e0, m, base + ch);
+    value_chunk<kCells>(sm, P, q, out, f, e0, m, base + ch, lb_key0, lb_key1);
     if (threadIdx.x == 0) {
       int n_active = n_active_lb;
       bool stalled = false;
