@@ -344,24 +344,43 @@ __global__ void __launch_bounds__(256) score_lb_kernel(const FrameDev* __restric
   // (the value grid, launched programmatically after this one, waits for it)
   asm volatile("griddepcontrol.launch_dependents;");
   if (f >= n_frames) return;
+  const FrameDev& F = frames[f];
   const int n = static_cast<int>(fc[f].q_count);
-  FrameDev F;  // only the field sizes are read
-  F.L = frames[f].L;
-  F.gw = frames[f].gw;
   unsigned long long best[2] = {0ull, 0ull};
+  int at[2] = {-1, -1};
   for (int e = lane; e < n; e += 32) {
     const int64_t pos = f * q.cap + e;
     double lo;
     score_bounds<true>(q.rx[pos], q.ry[pos], q.ot[pos], q.pt[pos], F, P, &lo, nullptr);
     const unsigned long long k = score_key(lo);
     const int s = q.slot[pos];
-    best[s] = k > best[s] ? k : best[s];
+    if (k > best[s]) {
+      best[s] = k;
+      at[s] = e;
+    }
   }
   for (int s = 0; s < 2; ++s) {
     const unsigned hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(best[s] >> 32));
     const unsigned lo = __reduce_max_sync(
         0xffffffffu, static_cast<unsigned>(best[s] >> 32) == hi ? static_cast<unsigned>(best[s]) : 0u);
-    if (lane == 0) fc[f].lb_key[s] = (static_cast<unsigned long long>(hi) << 32) | lo;
+    const unsigned long long key = (static_cast<unsigned long long>(hi) << 32) | lo;
+    // The slot's most promising cell gets its exact score (the same
+    // goal_view + score_pass the value kernel runs): the slot's best_pass is
+    // at least that, so it is a far tighter bound than the cell's own lower
+    // bound.  (A small slack keeps it a bound even if a last ulp differed.)
+    const unsigned owner = __ballot_sync(0xffffffffu, key != 0ull && best[s] == key);
+    unsigned long long out = key;
+    if (owner && lane == __ffs(owner) - 1) {
+      const int64_t pos = f * q.cap + at[s];
+      const double rx = q.rx[pos], ry = q.ry[pos];
+      const View v = goal_view_thread(rx, ry, F, P.radius, P.r_lt2, P.mb_le2, P.exact_only != 0);
+      double feat[5];
+      const double sc = score_from_view(v, rx, ry, q.ot[pos], q.pt[pos], F, P, feat);
+      const unsigned long long k2 = score_key(sc - (1e-9 + 1e-12 * fabs(sc)));
+      out = k2 > key ? k2 : key;
+    }
+    out = __shfl_sync(0xffffffffu, out, owner ? __ffs(owner) - 1 : 0);
+    if (lane == 0) fc[f].lb_key[s] = out;
   }
 }
 
