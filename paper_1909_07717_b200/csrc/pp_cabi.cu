@@ -600,7 +600,10 @@ cudaError_t query_occupancy(pp_ctx* ctx) {
 // tiles, and every scan CTA has started before any value CTA runs (the scan
 // triggers griddepcontrol.launch_dependents first thing), so they all finish.
 // Value CTAs per frame of a batch launch (each loops over the frame's chunks).
-constexpr int kValueCtasPerFrame = 16;
+#ifndef PP_VALUE_CTAS_PER_FRAME
+#define PP_VALUE_CTAS_PER_FRAME 8
+#endif
+constexpr int kValueCtasPerFrame = PP_VALUE_CTAS_PER_FRAME;
 
 int64_t value_wide_limit(const pp_ctx* ctx) {
   return static_cast<int64_t>(ctx->n_sms) * std::max(ctx->occ_value_wide, 4);

@@ -42,10 +42,28 @@ def _compact_of(s: abi.DppsSummary):
             [int(s.n_feasible[k]) for k in range(3)])
 
 
-@pytest.mark.parametrize("chip", [0, 1])
-def test_batch_equals_single_frame(ctx, chip):
+def _weighted(p, kind):
+    """Weight sets for the batch's score-bound pruning (every sign of the view
+    and refraction terms, custom norm bounds, a near-flat score)."""
+    w = p.pass_weights
+    if kind == "negative":
+        w.shoot_angle, w.refraction, w.teammate_time = -2.0, -1.5, -0.3
+    elif kind == "norms":
+        p.norm.length_upper, p.norm.angle_upper = 5.0, 0.7
+        w.margin, w.dist_goal = 0.05, -2.0
+    elif kind == "flat":
+        w.teammate_time = w.dist_goal = w.margin = 0.0
+        w.shoot_angle, w.refraction = 1e-3, 1e-3
+    return p
+
+
+@pytest.mark.parametrize("chip,weights", [(0, "default"), (1, "default"), (0, "negative"),
+                                          (1, "norms"), (0, "flat")])
+def test_batch_equals_single_frame(ctx, chip, weights):
+    """Batches prune cells by score bounds before the value function; the
+    single-frame path scores every cell: the results must be identical."""
     lib = abi.load_library()
-    p = _params()
+    p = _weighted(_params(), weights)
     grid = abi.SearchGrid(128, 64, 1.0, 6.5, 1, chip)
     n = 64
     frames_np = _mixed_frames(n, 100 + chip)
