@@ -7,8 +7,9 @@ oracles::random_world(mt19937_64(0xB200 + i), 8, 8) (proj/tests/oracles.hpp:
 228-258; regenerated bit for bit by paper_1909_07717_b200/synthetic.py), the
 SPEC default 128 directions x 64 kick speeds, flat (C1 grid: 8,192 cells x 16
 robots = 131,072 pass evaluations per frame), kicker = the teammate nearest
-the ball.  Every frame gets the full search, the value function of every
-feasible cell and best_pass for all / flat / chip.
+the ball.  Every frame gets the full search and an exact best_pass for all /
+flat / chip (the value function of every feasible cell whose score bound
+does not rule it out; results identical to scoring them all).
 
   value  pass evaluations/s over the whole batch, device-resident: the raw
          frames sit in HBM; one step stages them (id sort, kicker), builds
@@ -58,8 +59,10 @@ C5_PAIRS_PER_FRAME = C5_CELLS * 16  # cells x robots (kicker counted), = sbip_ca
 C2_PAIRS = 128 * 64 * 2 * 16
 CONFIG = {
     "workload": "configs[4] C5: 65,536 random 8v8 frames sharded over the GPUs; per frame "
-                "run_dpps (128x64 grid, flat) + score_pass of every feasible cell + best_pass "
-                "all/flat/chip",
+                "run_dpps (128x64 grid, flat: every cell x robot pair searched) + best_pass "
+                "all/flat/chip (exact: score_pass of every feasible cell that could be the "
+                "best -- cells whose score upper bound is below a scored cell's are skipped, "
+                "DESIGN 3.2)",
     "frames": C5_FRAMES,
     "frames_source": "oracles::random_world(mt19937_64(0xB200+i), 8, 8) (proj/tests/oracles.hpp)",
     "grid": "128 directions x 64 powers, flat (C1)",
