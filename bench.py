@@ -453,7 +453,8 @@ def run_ours(args, rank, world_size, local_rank):
         # dominant kernel: scan_kernel (the SBIP search the W_pair figure counts)
         pairs_local = n_local * C5_PAIRS_PER_FRAME
         achieved = w_pair * pairs_local / (scan_ms.value / 1e3) / 1e12
-        n_steps_launch = 2 + 2 * int(n_launch.value)  # stage + consts + (scan + value) per group
+        # stage + consts, then per group of frames: scan, score lower bounds, value
+        n_steps_launch = 2 + 3 * int(n_launch.value)
         out_line = {
             "metric": METRIC, "value": value, "unit": "pair-evals/s", "n_gpus": world_size,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
