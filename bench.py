@@ -476,7 +476,7 @@ def run_ours(args, rank, world_size, local_rank):
                              "dram_bytes_per_launch"),
                          "kernel": "scan_kernel (SBIP search, batch shape)",
                          "kernel_ms": {"stage+consts": stage_ms.value, "scan": scan_ms.value,
-                                       "value": value_ms.value,
+                                       "value (incl. score-bound pre-pass)": value_ms.value,
                                        "scan_launches": int(n_launch.value)},
                          "note": f"algorithmic FLOP = W_pair {w_pair:.1f}/pair (SURVEY 8(d) "
                                  f"formula, counted on C5 frames: profiles/c5_work.json) x "

@@ -688,14 +688,15 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   scfg.stream = ctx->stream;
   cudaError_t e = cudaLaunchKernelEx(&scfg, sfn, frames, P, co, q, fc, arg);
   if (e != cudaSuccess) return e;
+  if (mid) cudaEventRecord(mid, ctx->stream);
   if (!kCells) {
     // batches: the per-frame score lower bounds the value grid prunes with
+    // (timed with the value grid)
     pp::score_lb_kernel<<<static_cast<unsigned>((n_frames * 32 + 255) / 256), 256, 0,
                           ctx->stream>>>(frames, P, q, fc, n_frames);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  if (mid) cudaEventRecord(mid, ctx->stream);
   // Few chunks (one frame): wider CTAs shorten each chunk's chain of
   // dependent items; many chunks: narrower CTAs pack the SMs better.
   const unsigned vctas = static_cast<unsigned>(n_frames * chunks);
