@@ -2152,6 +2152,9 @@ extern "C" int pp_debug_champ_records(long long* out) {
 extern "C" int pp_debug_d1_records(long long* out) {
   return cudaMemcpyFromSymbol(out, pp::g_d1_rec, sizeof(pp::g_d1_rec)) == cudaSuccess ? 0 : -1;
 }
+extern "C" int pp_debug_d2_records(long long* out) {
+  return cudaMemcpyFromSymbol(out, pp::g_d2_rec, sizeof(pp::g_d2_rec)) == cudaSuccess ? 0 : -1;
+}
 extern "C" int pp_debug_win_records(long long* out) {
   return cudaMemcpyFromSymbol(out, pp::g_win_rec, sizeof(pp::g_win_rec)) == cudaSuccess ? 0 : -1;
 }

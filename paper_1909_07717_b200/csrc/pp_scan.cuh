@@ -262,6 +262,20 @@ __device__ long long g_d1_rec[512][256][2];
       g_d1_rec[blockIdx.x][pr][1] = pi.status + 4 * pi.fast + 8 * (pi.first >= 0); \
     }                                                                            \
   }
+// per value CTA and thread: D2 jobs, non-fast edges, band steps, exact
+// rounds, setup + first band run cycles, exact-round cycles
+__device__ long long g_d2_rec[512][256][6];
+#define PP_D2_DECL() \
+  long long d2st_[4] = {0, 0, 0, 0}; \
+  int d2jobs_ = 0, d2nf_ = 0
+#define PP_D2_ST d2st_
+#define PP_D2_JOB(fast) (++d2jobs_, d2nf_ += !(fast))
+#define PP_D2_FLUSH()                                                     \
+  if (blockIdx.x < 512 && threadIdx.x < 256) {                            \
+    long long* r_ = g_d2_rec[blockIdx.x][threadIdx.x];                    \
+    r_[0] = d2jobs_; r_[1] = d2nf_; r_[2] = d2st_[1]; r_[3] = d2st_[2];   \
+    r_[4] = d2st_[0]; r_[5] = d2st_[3];                                   \
+  }
 #define PP_TMARK(i) \
   if (threadIdx.x == 0) sm.tph[i] = clock64()
 __device__ long long g_champ_rec[kRecCtas][4];
@@ -309,6 +323,10 @@ __device__ long long g_warp_rec[kLaneRecCtas][16][4];  // plain / coop steps, cy
 #define PP_TMARK(i)
 #define PP_D1_T0()
 #define PP_D1_T1(pr, pi)
+#define PP_D2_DECL()
+#define PP_D2_ST nullptr
+#define PP_D2_JOB(fast)
+#define PP_D2_FLUSH()
 #define PP_CMARK(i)
 #define PP_CMARK_W(i)
 #define PP_ROBOT_START()

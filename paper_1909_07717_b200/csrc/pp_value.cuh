@@ -170,6 +170,7 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
   PP_MARK(3);
   // D2
   const int ns = sm.iv_n < kIvCap ? sm.iv_n : kIvCap;
+  PP_D2_DECL();
   for (int job = threadIdx.x; job < 2 * ns + 2 * m; job += blockDim.x) {
     if (job >= 2 * ns) {  // post angles of cell e (the sweep's fixed ends)
       const int e = (job - 2 * ns) >> 1, side = job & 1;
@@ -191,9 +192,10 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
         make_view_ctx(sm.q_rx[e], sm.q_ry[e], F, radius, P.r_lt2, P.mb_le2, hts, sm.n_half,
                       P.exact_only != 0);
     const int j = sm.iv_j[slot];
+    PP_D2_JOB(sm.iv_fast[slot]);
     const xd y = interval_edge_split(V, F.px[kTheirs + j], F.py[kTheirs + j], edge, sm.iv_first[slot],
                                sm.iv_last[slot], sm.iv_fast[slot], sm.iv_y1[slot], sm.iv_y2[slot],
-                               sm.iv_margin[slot]);
+                               sm.iv_margin[slot], PP_D2_ST);
     const double a = atan2((y - V.py).v, (V.gx - V.px).v);
     if (edge == 0) {
       sm.iv_lo[slot] = y.v;
@@ -204,6 +206,7 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
     }
   }
 
+  PP_D2_FLUSH();
   __syncthreads();
   PP_MARK(4);
   // D3a  thread per interval slot: the sweep's gap ending at this interval

@@ -28,6 +28,9 @@ CHAIN(datan2, double, 0.5, x = atan2(x, y) + 0.5)
 CHAIN(dsetp, double, 1.0, x = (x < y) ? __dadd_rn(x, 1e-9) : __dsub_rn(x, 1e-9))
 CHAIN(fsetp, float, 1.0f, x = (x < y) ? __fadd_rn(x, 1e-7f) : __fsub_rn(x, 1e-7f))
 CHAIN(dmidp, double, 1.0, x = __dmul_rn(0.5, __dadd_rn(x, y)); x = (x == y) ? 1.0 : x)
+// one integer bisection step: midpoint of two int64 ends, compare, select
+CHAIN(imid, long long, 1000000007LL, x = (x + (long long)y * 3 + 12345) >> 1; x = (x > 500000000LL) ? x : x + 777)
+CHAIN(iadd, long long, 1LL, x = x + (x >> 7) + 3)
 
 template <typename T>
 void run(const char* name, void (*k)(T*, long long*, int), int warps) {
@@ -56,6 +59,8 @@ int main() {
     run<double>("dsetp", k_dsetp, w);
     run<double>("dmidp", k_dmidp, w);
     run<float>("fsetp", k_fsetp, w);
+    run<long long>("imid", k_imid, w);
+    run<long long>("iadd", k_iadd, w);
     run<float>("fadd", k_fadd, w);
     run<float>("ffma", k_ffma, w);
     run<float>("fdiv", k_fdiv, w);
