@@ -131,7 +131,9 @@ struct ScanSmem {
   // A: per-cell window (lane = cell), raw storage (xd has a constructor)
   __align__(16) unsigned char cl_raw[32 * sizeof(CellLane)];
   int32_t ke[32];
-  int32_t cap[2][32];  // earliest hit sample per team and cell (team cap)
+  // earliest hit sample per team and cell (team cap); row 2: batches' cross
+  // cap of our team (cross_cap of their earliest hit)
+  int32_t cap[3][32];
   TrajF trf[32];  // FP32 trajectory per cell
   float2 win_s[32];  // FP32 ray distances of each cell's first / last window sample
   float2 tile_uf;  // FP32 unit direction of the tile
@@ -672,6 +674,35 @@ __device__ __forceinline__ int scan_start(const CellLane& c, const SampleF& S, f
   return k;
 }
 
+// Batches only (the outputs are the per-frame summary: feasible cells and the
+// best of them): once their team hits a cell at sample k (time tau =
+// k * dt), our robots need no sample j with fl(fl(j * dt) + safety) > tau --
+// a hit there, or the rest rule after it (time >= t_stop >= t_j), leaves
+// our time t with fl(t + safety) > tau >= their final time, an infeasible
+// cell (dpps.cpp:207-212) whatever our champion is; and where the cell is
+// feasible its champion hits at a sample j with fl(t_j + safety) <= their
+// final time <= tau, never cut.  Returns that largest useful j (-1: none;
+// every j when the safety margin allows all), rounding-exact: the estimate
+// is corrected with the reference's own FP64 comparison.
+__device__ __forceinline__ int cross_cap(int k, const DevParams& P) {
+  const xd dt = P.dt, sm = P.safety;
+  const xd tau = xd(double(k)) * dt;
+  auto ok = [&](int j) { return j < 0 || xd(double(j)) * dt + sm <= tau; };
+  const double est = floor((tau.v - sm.v) / dt.v);
+  if (!(est < 1e8)) return 0x7fffffff;  // (huge or NaN: no cut)
+  int j = est < -1.0 ? -1 : static_cast<int>(est);
+  for (int it = 0; it < 8; ++it) {
+    if (!ok(j)) {
+      --j;
+    } else if (ok(j + 1)) {
+      ++j;
+    } else {
+      return j;
+    }
+  }
+  return 0x7fffffff;  // (not settled: no cut)
+}
+
 // B of the scan for robot `ri` (one warp, lane = cell): scan_robot
 // (intercept.cpp:87-115) + first feasible sample (kernel.hpp:33-44) + rest
 // rule (dpps.cpp:177-190).  Two exact-safe accelerations, neither of which
@@ -688,7 +719,7 @@ __device__ __forceinline__ int scan_start(const CellLane& c, const SampleF& S, f
 // result is in *t_out / *code_out.
 // kEager: resolve the rest rule here (throughput shape, no extra pass);
 // else leave kNoHit for rest_rule_pass (latency shapes, final team caps).
-template <bool kEager>
+template <bool kEager, bool kX = false>
 __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_in, float2 win_s,
                                            const SampleF& S, const FrameDev& F, const DevParams& P,
                                            const RobotK& rk, int* cap,
@@ -713,6 +744,12 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
   // scanning.  Team caps are re-read from shared memory every step.
   const int team = F.scan_slot[ri] >= kTheirs ? 1 : 0;
   volatile int* vcap = cap + team * 32 + lane;
+  // kX (batches): our robots also stop past the cross cap (cap row 2)
+  volatile int* vxcap = cap + (kX && team == 0 ? 2 : team) * 32 + lane;
+  auto hit_at = [&](int kh) {
+    atomicMin(&cap[team * 32 + lane], kh);
+    if (kX && team == 1) atomicMin(&cap[2 * 32 + lane], cross_cap(kh, P));
+  };
   for (int n_step = 0; n_step < max_steps; ++n_step) {
     const unsigned act = __ballot_sync(0xffffffffu, state == 0);
 #ifdef PP_SCAN_STATS
@@ -731,7 +768,7 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
         if (exact_hit(c, F, P, robot_x(F, P, rk, ri), k)) {
           PP_STAT(9);
           hit = k;
-          atomicMin(&cap[team * 32 + lane], k);
+          hit_at(k);
           state = 2;
         } else {
           ++k;
@@ -747,7 +784,8 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
       ++n_tests;
 #endif
       int next = k;
-      const int code = test_sample(rk, S, k, trf, ke, *vcap, &next);
+      const int cap_c = kX ? min(*vcap, *vxcap) : *vcap;
+      const int code = test_sample(rk, S, k, trf, ke, cap_c, &next);
       switch (code) {
         case kRej:
           PP_CNT(c_skip);
@@ -758,7 +796,7 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
         case kHit:
           PP_CNT(c_ub);
           hit = k;
-          atomicMin(&cap[team * 32 + lane], k);
+          hit_at(k);
           state = 2;
           break;
         default: state = 1; break;  // kCand
@@ -1010,6 +1048,11 @@ __device__ __forceinline__ void tile_champions(const CellLane& c, const FrameDev
       PP_CMARK(3);
 }
 
+#ifndef PP_CROSS_CAP
+#define PP_CROSS_CAP 1
+#endif
+constexpr bool kCrossCap = PP_CROSS_CAP != 0;  // dev knob: batches' cross-team cap
+
 template <bool kCells, bool kLeftovers>
 __device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, const CellOut& out,
                                           const CellQueue& q, FrameCounters* __restrict__ fc,
@@ -1045,6 +1088,7 @@ __device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, cons
       reinterpret_cast<CellLane*>(sm.cl_raw)[lane] = c;
       sm.cap[0][lane] = 0x7fffffff;
       sm.cap[1][lane] = 0x7fffffff;
+      sm.cap[2][lane] = 0x7fffffff;
       if (lane == 0) {
         sm.n_left = 0;
         sm.next_pair = 0;
@@ -1106,6 +1150,9 @@ __device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, cons
         const float along = fmaxf(-(rk.bxf * u.x + rk.byf * u.y), 0.f);  // robot - ball on u
         const float ex = -rk.bxf - along * u.x, ey = -rk.byf - along * u.y;
         key = ex * ex + ey * ey;
+        // batches: their robots first, so the cross cap is set early
+        // (ours then still go nearest first among themselves)
+        if (kCrossCap && !kCells && F.scan_slot[lane] < kTheirs) key += 1e6f;
       }
       // (lanes >= n_scan hold the largest key: ranks of the scanned robots
       // only count the scanned robots)
@@ -1130,7 +1177,8 @@ __device__ __forceinline__ void scan_tile(ScanSmem& sm, const DevParams& P, cons
       double time;
       int code, lk;
       PP_ROBOT_START();
-      scan_robot<!kLeftovers>(cl[lane], sm.trf[lane], sm.win_s[lane], S, F, P, rk, &sm.cap[0][0], ri,
+      scan_robot<!kLeftovers, !kCells && !kLeftovers && kCrossCap>(
+                 cl[lane], sm.trf[lane], sm.win_s[lane], S, F, P, rk, &sm.cap[0][0], ri,
                  max_steps, &time,
                  &code, &lk);
       // an open pair: NaN time (no result is NaN) and its next sample

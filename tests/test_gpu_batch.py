@@ -44,8 +44,11 @@ def _compact_of(s: abi.DppsSummary):
 
 def _weighted(p, kind):
     """Weight sets for the batch's score-bound pruning (every sign of the view
-    and refraction terms, custom norm bounds, a near-flat score)."""
+    and refraction terms, custom norm bounds, a near-flat score), and safety
+    margins for the batch scan's cross-team cap (zero, off the sample grid, large)."""
     w = p.pass_weights
+    if kind.startswith("safety"):
+        p.thresholds.safety_margin = {"safety0": 0.0, "safety_odd": 0.0137, "safety_big": 0.7}[kind]
     if kind == "negative":
         w.shoot_angle, w.refraction, w.teammate_time = -2.0, -1.5, -0.3
     elif kind == "norms":
@@ -58,10 +61,12 @@ def _weighted(p, kind):
 
 
 @pytest.mark.parametrize("chip,weights", [(0, "default"), (1, "default"), (0, "negative"),
-                                          (1, "norms"), (0, "flat")])
+                                          (1, "norms"), (0, "flat"), (0, "safety0"),
+                                          (1, "safety_odd"), (0, "safety_big")])
 def test_batch_equals_single_frame(ctx, chip, weights):
-    """Batches prune cells by score bounds before the value function; the
-    single-frame path scores every cell: the results must be identical."""
+    """Batches prune cells by score bounds before the value function, and
+    their scans cut our robots past the cross-team cap; the single-frame path
+    scores every cell and scans fully: the results must be identical."""
     lib = abi.load_library()
     p = _weighted(_params(), weights)
     grid = abi.SearchGrid(128, 64, 1.0, 6.5, 1, chip)
