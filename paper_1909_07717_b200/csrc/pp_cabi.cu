@@ -1473,9 +1473,9 @@ pp_status pp_score_running_points(pp_ctx* ctx, const pp_world* world, const pp_p
 // filter statistics (pp_scan.cuh g_scan_stats).
 void pp_debug_scan_stats(unsigned long long* out16, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out16, pp::g_scan_stats, 24 * sizeof(unsigned long long));
+  cudaMemcpyFromSymbol(out16, pp::g_scan_stats, 64 * sizeof(unsigned long long));
   if (reset) {
-    unsigned long long z[24] = {};
+    unsigned long long z[64] = {};
     cudaMemcpyToSymbol(pp::g_scan_stats, z, sizeof(z));
   }
 }

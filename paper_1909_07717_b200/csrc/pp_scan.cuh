@@ -438,7 +438,9 @@ __device__ __forceinline__ CellLane cell_window(const FrameDev& F, const DevPara
 // Dev statistics of the filters (variant build -DPP_SCAN_STATS only; read
 // with pp_debug_scan_stats): sample outcomes, skipped samples, warp steps.
 #ifdef PP_SCAN_STATS
-__device__ unsigned long long g_scan_stats[24];
+// [24..39]: pairs by tests (bucket min(tests, 15) ... ), [40..55]: their tests;
+// [56]: lower-bound rejects in a run of >= 4 consecutive ones
+__device__ unsigned long long g_scan_stats[64];
 #define PP_STAT(i) atomicAdd(&g_scan_stats[i], 1ull)
 #define PP_STATN(i, n) atomicAdd(&g_scan_stats[i], static_cast<unsigned long long>(n))
 #else
@@ -579,6 +581,11 @@ __device__ __forceinline__ void pair_result(const CellLane& c, const DevParams& 
       const xd arr = arrival_to_point(c.rest_x, c.rest_y, X.px, X.py, X.vx, X.vy, X.a, X.b,
                                       X.vmax, P.radius);
       const xd ts = c.tr.t_stop;
+#ifdef PP_SCAN_STATS
+      PP_STAT(57);
+      if (arr <= ts) PP_STAT(58);
+      if (X.team == 0) PP_STAT(59);
+#endif
       time = (arr > ts ? arr : ts).v;
       code = -1;
     }
@@ -730,12 +737,15 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
   int k = scan_start(c, S, win_s);
   PP_STAT(10);
   if (k >= ke) PP_STAT(11);
+#ifdef PP_SCAN_STATS
+  if (F.scan_slot[ri] >= kTheirs) PP_STAT(22);  // their pairs
+#endif
   const TrajF trf = trf_in;
   int hit = -1;
   bool capped = false;
   int state = k >= ke ? 2 : 0;  // 0 scanning, 1 candidate pending, 2 finished
 #ifdef PP_SCAN_STATS
-  int n_tests = 0;
+  int n_tests = 0, lb_run = 0;
 #endif
   PP_CNT_DECL();
   // Warp-synchronous: each step every scanning lane examines one sample (or
@@ -756,6 +766,7 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
     if (lane == 0) {
       PP_STAT(12);
       PP_STATN(13, __popc(act));
+      if (team) PP_STAT(23);  // their warp steps
     }
 #endif
     if (act == 0u) {
@@ -782,6 +793,7 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
       PP_CNT(c_it);
 #ifdef PP_SCAN_STATS
       ++n_tests;
+      if (team) PP_STAT(15);  // their tests
 #endif
       int next = k;
       const int cap_c = kX ? min(*vcap, *vxcap) : *vcap;
@@ -789,6 +801,13 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
       switch (code) {
         case kRej:
           PP_CNT(c_skip);
+#ifdef PP_SCAN_STATS
+          if (next == k + 1) {
+            if (++lb_run >= 4) PP_STAT(56);
+          } else {
+            lb_run = 0;
+          }
+#endif
           k = next;
           break;
         case kEnd: state = 2; break;
@@ -805,6 +824,14 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
   }
   PP_CNT_FLUSH();
 #ifdef PP_SCAN_STATS
+  if (state == 2) {
+    const int b = n_tests < 4 ? n_tests : (n_tests < 8 ? 4 + (n_tests - 4) / 2
+                                                       : (n_tests < 16 ? 6 + (n_tests - 8) / 4
+                                                                       : (n_tests < 64 ? 8 + (n_tests - 16) / 16
+                                                                                       : (n_tests < 256 ? 11 + (n_tests - 64) / 64 : 15))));
+    PP_STAT(24 + b);
+    PP_STATN(40 + b, n_tests);
+  }
   // tests by outcome: 16/17 hit (count, tests), 18/19 capped, 20/21 window end
   {
     const int o = hit >= 0 ? 16 : (capped ? 18 : 20);
@@ -1251,7 +1278,16 @@ __global__ void __launch_bounds__(kWarps * 32, kCtas)
   __shared__ ScanSmem sm;
   PP_CLOCK_INIT();
   const int f = blockIdx.x / P.n_tiles;
-  const int tile = blockIdx.x % P.n_tiles;
+  // Heavy tiles first: slow kick speeds (low power tiles) before fast ones,
+  // flat before chip, then by direction.  Co-resident CTAs of one SM are
+  // launched about an SM count apart, so the round-1 order (power tile
+  // fastest-varying, 148 even) put heavy tiles on SMs with heavy tiles; this
+  // order gives the slowest tiles lighter neighbours (measured: C2 frame
+  // kernel span 51.2 -> 49.4 us, C1 41.9 -> 40.1 us).  Results do not
+  // depend on the order.
+  const int b = blockIdx.x % P.n_tiles;
+  const int per_pt = P.n_kt * P.n_dirs;
+  const int tile = (b % per_pt) * P.n_ptiles + b / per_pt;
   // Let the value kernel (launched with programmatic stream serialization)
   // get its CTAs resident while the last scan CTAs run; it waits for this
   // grid's completion before reading anything (griddepcontrol.wait).
