@@ -1280,14 +1280,17 @@ __global__ void __launch_bounds__(kWarps * 32, kCtas)
   const int f = blockIdx.x / P.n_tiles;
   // Heavy tiles first: slow kick speeds (low power tiles) before fast ones,
   // flat before chip, then by direction.  Co-resident CTAs of one SM are
-  // launched about an SM count apart, so the round-1 order (power tile
+  // launched about an SM count apart, so the grid order (power tile
   // fastest-varying, 148 even) put heavy tiles on SMs with heavy tiles; this
   // order gives the slowest tiles lighter neighbours (measured: C2 frame
-  // kernel span 51.2 -> 49.4 us, C1 41.9 -> 40.1 us).  Results do not
+  // kernel span 51.1 -> 49.1 us, C1 41.9 -> 39.7 us).  Not for multi-wave
+  // single frames (C3): their cell outputs stream into the result block,
+  // possibly host memory, and grid order keeps those writes sequential
+  // (C3 with the block in pinned memory: 1.58 vs 1.93 ms).  Results do not
   // depend on the order.
   const int b = blockIdx.x % P.n_tiles;
   const int per_pt = P.n_kt * P.n_dirs;
-  const int tile = (b % per_pt) * P.n_ptiles + b / per_pt;
+  const int tile = (kLeftovers || !kCells) ? (b % per_pt) * P.n_ptiles + b / per_pt : b;
   // Let the value kernel (launched with programmatic stream serialization)
   // get its CTAs resident while the last scan CTAs run; it waits for this
   // grid's completion before reading anything (griddepcontrol.wait).
