@@ -602,6 +602,7 @@ __device__ __forceinline__ void pair_result(const CellLane& c, const DevParams& 
 // whose time and id reach the outputs, dpps.cpp:192-213).  The team cap only
 // decreases, so reading it early is conservative.  cap_lane points at this
 // cell's entry of the team-cap table (cap_lane[team * 32]).
+template <bool kX = false>
 __device__ __forceinline__ void pair_finish(const CellLane& c, const FrameDev& F,
                                             const DevParams& P, const RobotK& rk, int ri,
                                             int hit, bool capped, const int* cap_lane,
@@ -613,6 +614,17 @@ __device__ __forceinline__ void pair_finish(const CellLane& c, const FrameDev& F
       *t_out = CUDART_INF;
       *code_out = -2;
       return;
+    }
+    if (kX && team == 0) {
+      // batches (see cross_cap): their hit at sample k_t leaves our rest-rule
+      // time t >= t_stop useless once fl(t_stop + safety) > k_t * dt
+      const int k_t = *reinterpret_cast<const volatile int*>(cap_lane + 32);
+      if (k_t != 0x7fffffff &&
+          c.tr.t_stop + xd(P.safety) > xd(double(k_t)) * xd(P.dt)) {
+        *t_out = CUDART_INF;
+        *code_out = -2;
+        return;
+      }
     }
   }
   pair_result(c, P, robot_x(F, P, rk, ri), hit, capped, t_out, code_out);
@@ -848,7 +860,7 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
   }
   *left_k = -1;
   if (kEager) {
-    pair_finish(c, F, P, rk, ri, hit, capped, cap + lane, t_out, code_out);
+    pair_finish<kX>(c, F, P, rk, ri, hit, capped, cap + lane, t_out, code_out);
   } else {
     pair_outcome(hit, capped, P, t_out, code_out);
   }
