@@ -686,7 +686,26 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   scfg.gridDim = dim3(static_cast<unsigned>(ctas));
   scfg.blockDim = dim3(32 * w);
   scfg.stream = ctx->stream;
-  cudaError_t e = cudaLaunchKernelEx(&scfg, sfn, frames, P, co, q, fc, arg);
+  // Many tiles (the throughput shape): a warp per tile (scan_warp_kernel),
+  // ~warp_tiles tiles per CTA.  Dev knobs: PP_WARP_TILES=n (0: the 4-warp
+  // tile CTAs of scan_kernel), PP_WARP_CELLS=0 (not for single frames).
+  static const int warp_tiles = [] {
+    const char* e = getenv("PP_WARP_TILES");
+    return e ? atoi(e) : 32;
+  }();
+  static const bool warp_cells = [] {
+    const char* e = getenv("PP_WARP_CELLS");
+    return e ? atoi(e) != 0 : true;
+  }();
+  pp::DevParams Ps = P;
+  if (warp_tiles > 0 && (!kCells || warp_cells) &&
+      sfn == pp::scan_kernel<kCells, pp::kScanWarpsNarrow, pp::kScanCtasNarrow>) {
+    Ps.scan_groups = std::max(1, P.n_tiles / warp_tiles);
+    sfn = pp::scan_warp_kernel<kCells, pp::kScanWarpWarps, pp::kScanWarpCtas>;
+    scfg.gridDim = dim3(static_cast<unsigned>(n_frames * Ps.scan_groups));
+    scfg.blockDim = dim3(32 * pp::kScanWarpWarps);
+  }
+  cudaError_t e = cudaLaunchKernelEx(&scfg, sfn, frames, Ps, co, q, fc, arg);
   if (e != cudaSuccess) return e;
   if (mid) cudaEventRecord(mid, ctx->stream);
   if (!kCells) {
@@ -728,7 +747,7 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
                            : pp::value_kernel<kCells, pp::kValueThreads>;
   cfg.blockDim = dim3(wide ? pp::kValueThreadsWide : pp::kValueThreads);
   if (rec)
-    *rec = PipeRec{frames, P, co, q, fc, parts, sums, nch, per_frame, sfn, vfn,
+    *rec = PipeRec{frames, Ps, co, q, fc, parts, sums, nch, per_frame, sfn, vfn,
                    scfg.gridDim, scfg.blockDim, cfg.gridDim, cfg.blockDim};
   return cudaLaunchKernelEx(&cfg, vfn, frames, P, q, fc, co, parts, sums, nch, per_frame,
                             arg.frame);

@@ -80,7 +80,9 @@ struct DevParams {
   // 1: the single frame and its robots' filter constants come in the
   // kernels' FrameArg parameter (no copy: the call graph updates the kernel
   // nodes' parameters), 0: from `frames` / rk_pre in global memory.
-  int32_t frame_in_arg, pad3;
+  int32_t frame_in_arg;
+  // scan_warp_kernel: CTAs per frame (each runs every scan_groups-th tile)
+  int32_t scan_groups;
   // Batches: the frame fold writes this compact per-frame result (indexed
   // like the launch's frames) instead of the full pp_dpps_summary.
   pp_frame_summary* compact;

@@ -25,6 +25,14 @@ constexpr int kScanWarpsWide = 16, kScanCtasWide = 2;
 #endif
 constexpr int kScanWarpsNarrow = PP_SCAN_WARPS_NARROW, kScanCtasNarrow = PP_SCAN_CTAS_NARROW;
 constexpr int kScanWarpsMid = 8, kScanCtasMid = 4;  // one wave of up to 4 x 148 tiles
+#ifndef PP_SCAN_WARP_W
+#define PP_SCAN_WARP_W 4
+#endif
+#ifndef PP_SCAN_WARP_C
+#define PP_SCAN_WARP_C 8
+#endif
+// scan_warp_kernel (batches): warps per CTA and CTAs per SM
+constexpr int kScanWarpWarps = PP_SCAN_WARP_W, kScanWarpCtas = PP_SCAN_WARP_C;
 #ifndef PP_VALUE_CHUNK
 #define PP_VALUE_CHUNK 32
 #endif
@@ -84,8 +92,7 @@ struct CellQueue {
 struct CellLane {
   Traj tr;
   double ux, uy;          // unit direction
-  double ax, ay, bx, by;  // first / last sample of the window (prune)
-  double s_lo, s_hi;      // ... and their distances along the ray
+  double s_lo, s_hi;      // ray distances of the window's first / last sample
   double rest_x, rest_y;  // rest point
   int kb, ke;             // window [kb, ke)
   bool valid, rif;        // power exists / ball rests in the field
@@ -420,17 +427,12 @@ __device__ __forceinline__ CellLane cell_window(const FrameDev& F, const DevPara
   c.rif = rif;
   c.rest_x = (ox + ux * tr.d_stop).v;
   c.rest_y = (oy + uy * tr.d_stop).v;
-  c.ax = c.ay = c.bx = c.by = 0.0;
   c.s_lo = c.s_hi = 0.0;
   if (kb < ke) {
     const xd s_lo = distance_at(tr, slide, roll, xd(double(kb)) * dt);
     const xd s_hi = distance_at(tr, slide, roll, xd(double(ke - 1)) * dt);
     c.s_lo = s_lo.v;
     c.s_hi = s_hi.v;
-    c.ax = (ox + ux * s_lo).v;
-    c.ay = (oy + uy * s_lo).v;
-    c.bx = (ox + ux * s_hi).v;
-    c.by = (oy + uy * s_hi).v;
   }
   return c;
 }
@@ -970,6 +972,14 @@ __device__ __forceinline__ void scan_leftovers(const CellLane* cl, const TrajF* 
   }
 }
 
+template <bool kCells>
+__device__ __forceinline__ void tile_publish(const CellLane& c, const FrameDev& F,
+                                             const DevParams& P, unsigned long long bt_o_bits,
+                                             int bk_o, int bs_o, unsigned long long bt_t_bits,
+                                             int bs_t, const CellOut& out, const CellQueue& q,
+                                             FrameCounters* __restrict__ fc, int f, int kt,
+                                             int64_t cell0);
+
 // C of the scan (dpps.cpp:140-213), one warp, lane = cell: our and their
 // champion (strict (time, id) lexicographic argmin seeded with (kNever, -1),
 // so visiting order does not matter), receive point, feasibility; cell
@@ -981,8 +991,6 @@ __device__ __forceinline__ void tile_champions(const CellLane& c, const FrameDev
                                                const CellOut& out, const CellQueue& q,
                                                FrameCounters* __restrict__ fc, int f, int kt,
                                                int64_t cell0) {
-  const int lane = threadIdx.x & 31;
-  const xd dt = P.dt, slide = P.slide, roll = P.roll;
       // Times are >= 0 or +inf (never NaN, never -0), so their bit patterns
       // order like the values: the (time, id) argmin runs on integers.
       const int n_ours_scan = F.n_ours - 1;  // kicker excluded
@@ -1012,10 +1020,26 @@ __device__ __forceinline__ void tile_champions(const CellLane& c, const FrameDev
           bs_t = s;
         }
       }
+      PP_CMARK(1);
+      tile_publish<kCells>(c, F, P, bt_o_bits, bri_o >= 0 ? res_k(bri_o) : -2, bs_o, bt_t_bits,
+                           bs_t, out, q, fc, f, kt, cell0);
+}
+
+// The end of C for one lane (cell): from its champions -- our (time bits,
+// hit code, slot) and theirs (time bits, index among theirs) -- the receive
+// point and feasibility (dpps.cpp:192-213), the append of a feasible cell to
+// the frame's value queue, and the cell outputs.
+template <bool kCells>
+__device__ __forceinline__ void tile_publish(const CellLane& c, const FrameDev& F,
+                                             const DevParams& P, unsigned long long bt_o_bits,
+                                             int bk_o, int bs_o, unsigned long long bt_t_bits,
+                                             int bs_t, const CellOut& out, const CellQueue& q,
+                                             FrameCounters* __restrict__ fc, int f, int kt,
+                                             int64_t cell0) {
+      const int lane = threadIdx.x & 31;
+      const xd dt = P.dt, slide = P.slide, roll = P.roll;
       const xd bt_o = __longlong_as_double(static_cast<long long>(bt_o_bits));
       const xd bt_t = __longlong_as_double(static_cast<long long>(bt_t_bits));
-      const int bk_o = bri_o >= 0 ? res_k(bri_o) : -2;
-      PP_CMARK(1);
       xd rx = 0.0, ry = 0.0;
       bool feas = false;
       if (bt_o.v < CUDART_INF) {
@@ -1337,6 +1361,168 @@ __global__ void __launch_bounds__(kWarps * 32, kCtas)
   }
 #endif
   PP_FLUSH(8);
+}
+
+// ---- throughput scan: a warp per tile ------------------------------------
+// Batches (and other launches of many tiles) have more tiles than the GPU
+// has warps, so a tile needs no more than one warp: the warp computes its
+// cells' windows (lane = cell), scans the tile's robots one after another,
+// keeps each cell's champions as it goes, and publishes the cells -- with no
+// CTA barrier between the phases (in the 4-warp-per-tile form, 3 of 4 warps
+// waited at barriers through the window and champion phases, and for the
+// tile's slowest robot).  Robots scanned in sequence also see their team's
+// final cap from every robot before them.  A CTA stages one frame and its
+// robots' constants once and its warps pull that frame's tiles (group g of
+// G: tiles g, g + G, ... in heavy-first order) from a shared counter.
+struct WarpTile {
+  __align__(16) unsigned char cl_raw[32 * sizeof(CellLane)];
+  TrajF trf[32];
+  float2 win_s[32];
+  int32_t cap[3][32];  // team caps (ours, theirs) and our cross cap, per cell
+};
+
+template <int kWarps>
+struct ScanWarpSmem {
+  RobotK rk[kMaxRobots];
+  FrameDev frame;
+  unsigned next_tile;
+  WarpTile w[kWarps];
+};
+
+template <bool kCells>
+__device__ __forceinline__ void warp_tile(const FrameDev& F, const RobotK* rk_s, WarpTile& ws,
+                                          const DevParams& P, const CellOut& out,
+                                          const CellQueue& q, FrameCounters* __restrict__ fc,
+                                          int f, int tile) {
+  const int lane = threadIdx.x & 31;
+  const int kt = tile / (P.n_dirs * P.n_ptiles);
+  const int dir = (tile / P.n_ptiles) % P.n_dirs;
+  const int ptile = tile % P.n_ptiles;
+  const int pw = ptile * 32 + lane;
+  const int64_t cell0 = (static_cast<int64_t>(kt) * P.n_dirs + dir) * P.n_pows + ptile * 32;
+  // A: the window of this lane's cell (as scan_tile)
+  {
+    const double4 dd = P.dirs[dir];
+    const PowRow pr = P.pows[kt * P.n_pows + (pw < P.n_pows ? pw : P.n_pows - 1)];
+    const CellLane c = cell_window(F, P, dd, pr, pw < P.n_pows);
+    reinterpret_cast<CellLane*>(ws.cl_raw)[lane] = c;
+    ws.trf[lane] = TrajF(c.tr, static_cast<float>(P.slide), static_cast<float>(P.roll));
+    ws.win_s[lane] = make_float2(static_cast<float>(c.s_lo), static_cast<float>(c.s_hi));
+    ws.cap[0][lane] = ws.cap[1][lane] = ws.cap[2][lane] = 0x7fffffff;
+  }
+  const float2 uf = make_float2(static_cast<float>(P.dirs[dir].z), static_cast<float>(P.dirs[dir].w));
+  __syncwarp();
+  const CellLane& c = reinterpret_cast<const CellLane*>(ws.cl_raw)[lane];
+  // Robot order: their robots first (their hits set our cross cap), then
+  // nearest the tile's ray first (the longest scans and earliest team caps).
+  // Lane = robot; order does not change results.
+  int my_rank = 0;
+  {
+    float key = 3.0e38f;
+    if (lane < F.n_scan) {
+      const RobotK& rk = rk_s[lane];
+      const float along = fmaxf(-(rk.bxf * uf.x + rk.byf * uf.y), 0.f);
+      const float ex = -rk.bxf - along * uf.x, ey = -rk.byf - along * uf.y;
+      key = ex * ex + ey * ey;
+      if (kCrossCap && !kCells && F.scan_slot[lane] < kTheirs) key += 1e6f;
+    }
+    for (int j = 0; j < F.n_scan; ++j) {
+      const float kj = __shfl_sync(0xffffffffu, key, j);
+      my_rank += (kj < key || (kj == key && j < lane)) ? 1 : 0;
+    }
+  }
+  // B: every robot in rank order, this lane's champions -- (time bits, id)
+  // argmin per team, as tile_champions -- updated after each
+  unsigned long long bt_o = 0x7ff0000000000000ull, bt_t = 0x7ff0000000000000ull;  // +inf
+  int bid_o = -1, bk_o = -2, bs_o = -1, bid_t = -1, bs_t = -1;
+  for (int i = 0; i < F.n_scan; ++i) {
+    const int ri = __ffs(__ballot_sync(0xffffffffu, my_rank == i)) - 1;
+    const RobotK& rk = rk_s[ri];
+    const SampleF S = sample_f(rk, uf, P);
+    double time;
+    int code, lk;
+    scan_robot<true, !kCells && kCrossCap>(c, ws.trf[lane], ws.win_s[lane], S, F, P, rk,
+                                           &ws.cap[0][0], ri, 1 << 30, &time, &code, &lk);
+    const int slot = F.scan_slot[ri];
+    const int id = F.id[slot];
+    const unsigned long long tb = __double_as_longlong(time);
+    if (slot < kTheirs) {
+      if (tb < bt_o || (tb == bt_o && id < bid_o)) {
+        bt_o = tb;
+        bid_o = id;
+        bk_o = code;
+        bs_o = slot;
+      }
+    } else if (tb < bt_t || (tb == bt_t && id < bid_t)) {
+      bt_t = tb;
+      bid_t = id;
+      bs_t = slot - kTheirs;
+    }
+  }
+  // C: receive point, feasibility, queue, cell outputs
+  tile_publish<kCells>(c, F, P, bt_o, bk_o, bs_o, bt_t, bs_t, out, q, fc, f, kt, cell0);
+  __syncwarp();  // (ws is reused by the warp's next tile)
+}
+
+// Grid: n_frames x P.scan_groups CTAs; CTA (f, g) runs its share of frame
+// f's tiles (below).
+template <bool kCells, int kWarps, int kCtas>
+__global__ void __launch_bounds__(kWarps * 32, kCtas)
+    scan_warp_kernel(const FrameDev* __restrict__ frames, DevParams P, CellOut out, CellQueue q,
+                     FrameCounters* __restrict__ fc, const __grid_constant__ FrameArg fa) {
+  __shared__ ScanWarpSmem<kWarps> sm;
+  const int groups = P.scan_groups;
+  const int f = blockIdx.x / groups;
+  const int g = blockIdx.x % groups;
+  asm volatile("griddepcontrol.launch_dependents;");
+  const FrameDev* src = P.frame_in_arg ? &fa.frame : frames + f;
+  const RobotK* rk_arg = P.frame_in_arg ? fa.rk : nullptr;
+  if (threadIdx.x == 0) {
+    atomicMax(&fc[f].t0_inv, ~pp_now_ns());
+    sm.next_tile = 0;
+  }
+  {
+    const int4* fs = reinterpret_cast<const int4*>(src);
+    int4* fd = reinterpret_cast<int4*>(&sm.frame);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(FrameDev) / 16); i += blockDim.x)
+      fd[i] = fs[i];
+  }
+  const int n_scan = src->n_scan;
+  if (rk_arg || P.rk_pre) {
+    const int4* rks = rk_arg ? reinterpret_cast<const int4*>(rk_arg)
+                             : static_cast<const int4*>(P.rk_pre) +
+                                   static_cast<int64_t>(f) * (kMaxRobots * sizeof(RobotK) / 16);
+    int4* dst = reinterpret_cast<int4*>(sm.rk);
+    const int n16 = n_scan * static_cast<int>(sizeof(RobotK) / 16);
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = rks[i];
+  } else if (static_cast<int>(threadIdx.x) < n_scan) {
+    robot_consts(*src, P, threadIdx.x, &sm.rk[threadIdx.x]);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  WarpTile& ws = sm.w[threadIdx.x >> 5];
+  // Batches: tiles g, g + groups, ... in heavy-first order (each CTA gets a
+  // mix of heavy and light tiles, heaviest first).  Cell outputs (a single
+  // multi-wave frame): a contiguous range of tiles in grid order, so the
+  // result block is written sequentially (it may be host memory).
+  const int per_cta = (P.n_tiles + groups - 1) / groups;
+  const int n_mine = kCells ? min(per_cta, P.n_tiles - g * per_cta)
+                            : (P.n_tiles - g + groups - 1) / groups;
+  const int per_pt = P.n_kt * P.n_dirs;
+  for (;;) {
+    unsigned j = 0;
+    if (lane == 0) j = atomicAdd(&sm.next_tile, 1u);
+    j = __shfl_sync(0xffffffffu, j, 0);
+    if (static_cast<int>(j) >= n_mine) break;
+    int tile;
+    if (kCells) {
+      tile = g * per_cta + static_cast<int>(j);
+    } else {
+      const int b = g + groups * static_cast<int>(j);
+      tile = (b % per_pt) * P.n_ptiles + b / per_pt;
+    }
+    warp_tile<kCells>(sm.frame, sm.rk, ws, P, out, q, fc, f, tile);
+  }
 }
 
 // robot_consts of every scanned robot of every frame of a batch, once
