@@ -130,6 +130,9 @@ struct pp_ctx {
   PinnedBuf frame_h;
   int dirs_n = -1;
   std::vector<double> pows_key;  // inputs the power table was built from
+  int max_count = 0;             // most samples of any power row
+  DevBuf xcap;                   // batches: cross_cap table (xcap_table_kernel)
+  std::vector<double> xcap_key;  // (dt, safety, entries) it was built for
   // run map
   DevBuf run_block, run_partials, run_counter;
   // batch: raw worlds (+ caller's kicker ids) uploaded, staged FrameDevs,
@@ -563,6 +566,8 @@ cudaError_t ensure_tables(pp_ctx* ctx, pp::DevParams* P) {
                           cudaMemcpyHostToDevice, ctx->stream);
     if (e != cudaSuccess) return e;
     ctx->pows_key = key;
+    ctx->max_count = 0;
+    for (const pp::PowRow& r : rows) ctx->max_count = std::max(ctx->max_count, r.count);
     ctx->last_valid = false;
   }
   P->dirs = static_cast<const double4*>(ctx->dirs.p);
@@ -698,6 +703,23 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
     return e ? atoi(e) != 0 : true;
   }();
   pp::DevParams Ps = P;
+  if (!kCells) {
+    // the cross caps of every sample index a hit can have (batches)
+    const std::vector<double> xkey = {P.dt, P.safety, double(ctx->max_count)};
+    if (xkey != ctx->xcap_key && ctx->max_count > 0) {
+      cudaError_t xe = ctx->xcap.reserve(ctx->stream, sizeof(int32_t) * ctx->max_count);
+      if (xe != cudaSuccess) return xe;
+      pp::xcap_table_kernel<<<(ctx->max_count + 255) / 256, 256, 0, ctx->stream>>>(
+          P, static_cast<int32_t*>(ctx->xcap.p), ctx->max_count);
+      xe = cudaGetLastError();
+      if (xe != cudaSuccess) return xe;
+      ctx->xcap_key = xkey;
+    }
+    if (ctx->xcap_key == xkey) {
+      Ps.xcap = static_cast<const int32_t*>(ctx->xcap.p);
+      Ps.n_xcap = ctx->max_count;
+    }
+  }
   if (warp_tiles > 0 && (!kCells || warp_cells) &&
       sfn == pp::scan_kernel<kCells, pp::kScanWarpsNarrow, pp::kScanCtasNarrow>) {
     Ps.scan_groups = std::max(1, P.n_tiles / warp_tiles);

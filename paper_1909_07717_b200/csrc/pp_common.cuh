@@ -83,6 +83,9 @@ struct DevParams {
   int32_t frame_in_arg;
   // scan_warp_kernel: CTAs per frame (each runs every scan_groups-th tile)
   int32_t scan_groups;
+  // Batches: cross_cap(k) for k < n_xcap (xcap_table_kernel), else nullptr
+  const int32_t* xcap;
+  int32_t n_xcap, pad4;
   // Batches: the frame fold writes this compact per-frame result (indexed
   // like the launch's frames) instead of the full pp_dpps_summary.
   pp_frame_summary* compact;

@@ -724,6 +724,17 @@ __device__ __forceinline__ int cross_cap(int k, const DevParams& P) {
   return 0x7fffffff;  // (not settled: no cut)
 }
 
+// cross_cap from the launch's table (DevParams::xcap, built by
+// xcap_table_kernel with cross_cap itself) where it covers k.
+__device__ __forceinline__ int cross_cap_t(int k, const DevParams& P) {
+  return k < P.n_xcap ? __ldg(P.xcap + k) : cross_cap(k, P);
+}
+
+__global__ void xcap_table_kernel(DevParams P, int32_t* __restrict__ tab, int n) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) tab[k] = cross_cap(k, P);
+}
+
 // B of the scan for robot `ri` (one warp, lane = cell): scan_robot
 // (intercept.cpp:87-115) + first feasible sample (kernel.hpp:33-44) + rest
 // rule (dpps.cpp:177-190).  Two exact-safe accelerations, neither of which
@@ -740,7 +751,10 @@ __device__ __forceinline__ int cross_cap(int k, const DevParams& P) {
 // result is in *t_out / *code_out.
 // kEager: resolve the rest rule here (throughput shape, no extra pass);
 // else leave kNoHit for rest_rule_pass (latency shapes, final team caps).
-template <bool kEager, bool kX = false>
+// kSolo (scan_warp_kernel): the warp is the cell's only scanner, so the
+// caps cannot move during this robot's scan except by its own hit (which
+// ends it): they are read once, and updated without atomics.
+template <bool kEager, bool kX = false, bool kSolo = false>
 __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_in, float2 win_s,
                                            const SampleF& S, const FrameDev& F, const DevParams& P,
                                            const RobotK& rk, int* cap,
@@ -771,9 +785,19 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
   // kX (batches): our robots also stop past the cross cap (cap row 2)
   volatile int* vxcap = cap + (kX && team == 0 ? 2 : team) * 32 + lane;
   auto hit_at = [&](int kh) {
-    atomicMin(&cap[team * 32 + lane], kh);
-    if (kX && team == 1) atomicMin(&cap[2 * 32 + lane], cross_cap(kh, P));
+    if (kSolo) {
+      int* ct = &cap[team * 32 + lane];
+      *ct = min(*ct, kh);
+      if (kX && team == 1) {
+        int* cx = &cap[2 * 32 + lane];
+        *cx = min(*cx, cross_cap_t(kh, P));
+      }
+    } else {
+      atomicMin(&cap[team * 32 + lane], kh);
+      if (kX && team == 1) atomicMin(&cap[2 * 32 + lane], cross_cap_t(kh, P));
+    }
   };
+  const int cap_solo = kSolo ? (kX ? min(*vcap, *vxcap) : *vcap) : 0;
   for (int n_step = 0; n_step < max_steps; ++n_step) {
     const unsigned act = __ballot_sync(0xffffffffu, state == 0);
 #ifdef PP_SCAN_STATS
@@ -810,7 +834,7 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
       if (team) PP_STAT(15);  // their tests
 #endif
       int next = k;
-      const int cap_c = kX ? min(*vcap, *vxcap) : *vcap;
+      const int cap_c = kSolo ? cap_solo : (kX ? min(*vcap, *vxcap) : *vcap);
       const int code = test_sample(rk, S, k, trf, ke, cap_c, &next);
       switch (code) {
         case kRej:
@@ -1381,6 +1405,7 @@ struct WarpTile {
   int32_t cap[3][32];  // team caps (ours, theirs) and our cross cap, per cell
 };
 
+
 template <int kWarps>
 struct ScanWarpSmem {
   RobotK rk[kMaxRobots];
@@ -1435,14 +1460,7 @@ __device__ __forceinline__ void warp_tile(const FrameDev& F, const RobotK* rk_s,
   // argmin per team, as tile_champions -- updated after each
   unsigned long long bt_o = 0x7ff0000000000000ull, bt_t = 0x7ff0000000000000ull;  // +inf
   int bid_o = -1, bk_o = -2, bs_o = -1, bid_t = -1, bs_t = -1;
-  for (int i = 0; i < F.n_scan; ++i) {
-    const int ri = __ffs(__ballot_sync(0xffffffffu, my_rank == i)) - 1;
-    const RobotK& rk = rk_s[ri];
-    const SampleF S = sample_f(rk, uf, P);
-    double time;
-    int code, lk;
-    scan_robot<true, !kCells && kCrossCap>(c, ws.trf[lane], ws.win_s[lane], S, F, P, rk,
-                                           &ws.cap[0][0], ri, 1 << 30, &time, &code, &lk);
+  auto champion = [&](int ri, double time, int code) {
     const int slot = F.scan_slot[ri];
     const int id = F.id[slot];
     const unsigned long long tb = __double_as_longlong(time);
@@ -1457,6 +1475,46 @@ __device__ __forceinline__ void warp_tile(const FrameDev& F, const RobotK* rk_s,
       bt_t = tb;
       bid_t = id;
       bs_t = slot - kTheirs;
+    }
+  };
+  constexpr bool kX = !kCells && kCrossCap;
+  unsigned rest_mask = 0;  // robots (bit ri) whose pair ended without a hit
+  for (int i = 0; i < F.n_scan; ++i) {
+    const int ri = __ffs(__ballot_sync(0xffffffffu, my_rank == i)) - 1;
+    const RobotK& rk = rk_s[ri];
+    const SampleF S = sample_f(rk, uf, P);
+    double time;
+    int code, lk;
+    scan_robot<false, kX, true>(c, ws.trf[lane], ws.win_s[lane], S, F, P, rk, &ws.cap[0][0], ri,
+                          1 << 30, &time, &code, &lk);
+    if (code >= 0) {
+      champion(ri, time, code);
+    } else if (code == kNoHit && c.valid && c.rif) {
+      rest_mask |= 1u << ri;
+    }
+    // (capped out, or no hit with the rest outside the field: +inf, which
+    // never displaces a champion)
+  }
+  // The rest rule (dpps.cpp:177-190) of the pairs without a hit, after every
+  // robot, with the lane's final caps: skipped where the robot's team hit
+  // strictly before the ball rests, and (batches) for ours where their hit
+  // leaves the cell infeasible anyway (pair_finish's rules; caps only
+  // decrease, so the final ones skip at least as much).
+  {
+    const int cap_o = ws.cap[0][lane], cap_t = ws.cap[1][lane];
+    while (rest_mask) {
+      const int rj = __ffs(rest_mask) - 1;
+      rest_mask &= rest_mask - 1;
+      const bool theirs = F.scan_slot[rj] >= kTheirs;
+      const int k_team = theirs ? cap_t : cap_o;
+      if ((k_team != 0x7fffffff && xd(double(k_team)) * xd(P.dt) < c.tr.t_stop) ||
+          (kX && !theirs && cap_t != 0x7fffffff &&
+           c.tr.t_stop + xd(P.safety) > xd(double(cap_t)) * xd(P.dt)))
+        continue;
+      double t;
+      int cd;
+      pair_result(c, P, robot_x(F, P, rk_s[rj], rj), -1, false, &t, &cd);
+      champion(rj, t, cd);
     }
   }
   // C: receive point, feasibility, queue, cell outputs
