@@ -29,7 +29,7 @@ constexpr int kScanWarpsMid = 8, kScanCtasMid = 4;  // one wave of up to 4 x 148
 #define PP_SCAN_WARP_W 4
 #endif
 #ifndef PP_SCAN_WARP_C
-#define PP_SCAN_WARP_C 8
+#define PP_SCAN_WARP_C 7
 #endif
 // scan_warp_kernel (batches): warps per CTA and CTAs per SM
 constexpr int kScanWarpWarps = PP_SCAN_WARP_W, kScanWarpCtas = PP_SCAN_WARP_C;
