@@ -1002,7 +1002,7 @@ __device__ __forceinline__ void tile_publish(const CellLane& c, const FrameDev& 
                                              int bk_o, int bs_o, unsigned long long bt_t_bits,
                                              int bs_t, const CellOut& out, const CellQueue& q,
                                              FrameCounters* __restrict__ fc, int f, int kt,
-                                             int64_t cell0);
+                                             int64_t cell);
 
 // C of the scan (dpps.cpp:140-213), one warp, lane = cell: our and their
 // champion (strict (time, id) lexicographic argmin seeded with (kNever, -1),
@@ -1046,7 +1046,7 @@ __device__ __forceinline__ void tile_champions(const CellLane& c, const FrameDev
       }
       PP_CMARK(1);
       tile_publish<kCells>(c, F, P, bt_o_bits, bri_o >= 0 ? res_k(bri_o) : -2, bs_o, bt_t_bits,
-                           bs_t, out, q, fc, f, kt, cell0);
+                           bs_t, out, q, fc, f, kt, cell0 + (threadIdx.x & 31));
 }
 
 // The end of C for one lane (cell): from its champions -- our (time bits,
@@ -1059,7 +1059,7 @@ __device__ __forceinline__ void tile_publish(const CellLane& c, const FrameDev& 
                                              int bk_o, int bs_o, unsigned long long bt_t_bits,
                                              int bs_t, const CellOut& out, const CellQueue& q,
                                              FrameCounters* __restrict__ fc, int f, int kt,
-                                             int64_t cell0) {
+                                             int64_t cell) {
       const int lane = threadIdx.x & 31;
       const xd dt = P.dt, slide = P.slide, roll = P.roll;
       const xd bt_o = __longlong_as_double(static_cast<long long>(bt_o_bits));
@@ -1078,7 +1078,6 @@ __device__ __forceinline__ void tile_publish(const CellLane& c, const FrameDev& 
         feas = isinf(bt_t.v) || (bt_o + xd(P.safety) <= bt_t);
       }
       feas = feas && c.valid;
-      const int64_t cell = cell0 + lane;
       PP_CMARK(2);
       const unsigned fm = __ballot_sync(0xffffffffu, feas);
       unsigned base = 0;
@@ -1420,16 +1419,17 @@ __device__ __forceinline__ void warp_tile(const FrameDev& F, const RobotK* rk_s,
                                           const CellQueue& q, FrameCounters* __restrict__ fc,
                                           int f, int tile) {
   const int lane = threadIdx.x & 31;
+  // lane = power: tile = (kick slot, direction, 32 powers)
   const int kt = tile / (P.n_dirs * P.n_ptiles);
   const int dir = (tile / P.n_ptiles) % P.n_dirs;
-  const int ptile = tile % P.n_ptiles;
-  const int pw = ptile * 32 + lane;
-  const int64_t cell0 = (static_cast<int64_t>(kt) * P.n_dirs + dir) * P.n_pows + ptile * 32;
+  const bool valid = (tile % P.n_ptiles) * 32 + lane < P.n_pows;
+  const int pw = valid ? (tile % P.n_ptiles) * 32 + lane : P.n_pows - 1;
+  const int64_t cell = (static_cast<int64_t>(kt) * P.n_dirs + dir) * P.n_pows + pw;
   // A: the window of this lane's cell (as scan_tile)
   {
     const double4 dd = P.dirs[dir];
-    const PowRow pr = P.pows[kt * P.n_pows + (pw < P.n_pows ? pw : P.n_pows - 1)];
-    const CellLane c = cell_window(F, P, dd, pr, pw < P.n_pows);
+    const PowRow pr = P.pows[kt * P.n_pows + pw];
+    const CellLane c = cell_window(F, P, dd, pr, valid);
     reinterpret_cast<CellLane*>(ws.cl_raw)[lane] = c;
     ws.trf[lane] = TrajF(c.tr, static_cast<float>(P.slide), static_cast<float>(P.roll));
     ws.win_s[lane] = make_float2(static_cast<float>(c.s_lo), static_cast<float>(c.s_hi));
@@ -1518,7 +1518,7 @@ __device__ __forceinline__ void warp_tile(const FrameDev& F, const RobotK* rk_s,
     }
   }
   // C: receive point, feasibility, queue, cell outputs
-  tile_publish<kCells>(c, F, P, bt_o, bk_o, bs_o, bt_t, bs_t, out, q, fc, f, kt, cell0);
+  tile_publish<kCells>(c, F, P, bt_o, bk_o, bs_o, bt_t, bs_t, out, q, fc, f, kt, cell);
   __syncwarp();  // (ws is reused by the warp's next tile)
 }
 
