@@ -474,7 +474,7 @@ def run_ours(args, rank, world_size, local_rank):
                          "unit": "TFLOP/s", "frac": achieved / peak_tflops,
                          "traffic": _load_json("profiles/ncu_summary.json").get(
                              "dram_bytes_per_launch"),
-                         "kernel": "scan_kernel (SBIP search, batch shape)",
+                         "kernel": "scan_warp_kernel (SBIP search, batch shape: a warp per tile)",
                          "kernel_ms": {"stage+consts": stage_ms.value, "scan": scan_ms.value,
                                        "value (incl. score-bound pre-pass)": value_ms.value,
                                        "scan_launches": int(n_launch.value)},
