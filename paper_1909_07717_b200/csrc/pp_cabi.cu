@@ -691,16 +691,19 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   scfg.gridDim = dim3(static_cast<unsigned>(ctas));
   scfg.blockDim = dim3(32 * w);
   scfg.stream = ctx->stream;
-  // Many tiles (the throughput shape): a warp per tile (scan_warp_kernel),
-  // ~warp_tiles tiles per CTA.  Dev knobs: PP_WARP_TILES=n (0: the 4-warp
-  // tile CTAs of scan_kernel), PP_WARP_CELLS=0 (not for single frames).
+  // Batches (the throughput shape): a warp per tile (scan_warp_kernel),
+  // ~warp_tiles tiles per CTA.  Not for a single multi-wave frame (the 1 cm
+  // grid): there it is no faster, and with the result block in pinned host
+  // memory the later, burstier tile completions cost (C3 1.48 -> 1.71 ms).
+  // Dev knobs: PP_WARP_TILES=n (0: the 4-warp tile CTAs of scan_kernel),
+  // PP_WARP_CELLS=1 (single frames too).
   static const int warp_tiles = [] {
     const char* e = getenv("PP_WARP_TILES");
     return e ? atoi(e) : 32;
   }();
   static const bool warp_cells = [] {
     const char* e = getenv("PP_WARP_CELLS");
-    return e ? atoi(e) != 0 : true;
+    return e ? atoi(e) != 0 : false;
   }();
   pp::DevParams Ps = P;
   if (!kCells) {

@@ -1559,26 +1559,20 @@ __global__ void __launch_bounds__(kWarps * 32, kCtas)
   __syncthreads();
   const int lane = threadIdx.x & 31;
   WarpTile& ws = sm.w[threadIdx.x >> 5];
-  // Batches: tiles g, g + groups, ... in heavy-first order (each CTA gets a
-  // mix of heavy and light tiles, heaviest first).  Cell outputs (a single
-  // multi-wave frame): a contiguous range of tiles in grid order, so the
-  // result block is written sequentially (it may be host memory).
-  const int per_cta = (P.n_tiles + groups - 1) / groups;
-  const int n_mine = kCells ? min(per_cta, P.n_tiles - g * per_cta)
-                            : (P.n_tiles - g + groups - 1) / groups;
+  // CTA g runs tiles g, g + groups, ...: batches in heavy-first order (each
+  // CTA gets a mix of heavy and light tiles, heaviest first); cell outputs (a
+  // single multi-wave frame) in grid order, so the tiles running at any time
+  // are neighbours and the result block (possibly host memory) is written
+  // about sequentially.
+  const int n_mine = (P.n_tiles - g + groups - 1) / groups;
   const int per_pt = P.n_kt * P.n_dirs;
   for (;;) {
     unsigned j = 0;
     if (lane == 0) j = atomicAdd(&sm.next_tile, 1u);
     j = __shfl_sync(0xffffffffu, j, 0);
     if (static_cast<int>(j) >= n_mine) break;
-    int tile;
-    if (kCells) {
-      tile = g * per_cta + static_cast<int>(j);
-    } else {
-      const int b = g + groups * static_cast<int>(j);
-      tile = (b % per_pt) * P.n_ptiles + b / per_pt;
-    }
+    const int b = g + groups * static_cast<int>(j);
+    const int tile = kCells ? b : (b % per_pt) * P.n_ptiles + b / per_pt;
     warp_tile<kCells>(sm.frame, sm.rk, ws, P, out, q, fc, f, tile);
   }
 }
