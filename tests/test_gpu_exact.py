@@ -143,3 +143,44 @@ def test_goal_views_and_possession_exact_only(ctx):
             res.append(bytes(got))
         lib.pp_ctx_set_option(ctx, abi.PP_OPT_EXACT_ONLY, 0)
         assert res[0] == res[1], cid
+
+
+@pytest.mark.timeout(900)
+def test_batch_razor_worlds_shortcuts_on_off_identical(ctx):
+    """The batch path (pp_dpps_frames: the warp-per-tile scan with caps read
+    once per robot, the deferred rest rule and the cross-cap table) on
+    razor-margin worlds and random 1..16 v 0..16 worlds: per-frame results
+    byte-identical with the FP32 shortcuts on and off, and equal to the
+    single-frame path's summary."""
+    lib = abi.load_library()
+    p = _params()
+    for grid in (abi.SearchGrid(128, 64, 1.0, 6.5, 1, 0), C2):
+        worlds, kickers = razor.razor_worlds(14, p, grid)
+        rnd = synthetic.random_worlds(np.arange(18, dtype=np.uint64) + np.uint64(4242), 16, 16)
+        rng = np.random.default_rng(5)
+        for i in range(rnd.shape[0]):
+            rnd["n_ours"][i] = int(rng.integers(2, 17))
+            rnd["n_theirs"][i] = int(rng.integers(0, 17))
+        fr = np.concatenate([worlds.astype(rnd.dtype), rnd])
+        n = fr.shape[0]
+        frames, _keep = synthetic.as_ctypes(fr)
+        kick = (C.c_int32 * n)(*([int(k) for k in kickers] +
+                                 [int(rnd["ours"]["id"][i][0]) for i in range(rnd.shape[0])]))
+        fast = (abi.FrameSummary * n)()
+        exact = (abi.FrameSummary * n)()
+        assert lib.pp_dpps_frames(ctx, frames, n, C.byref(p), C.byref(grid), kick, fast) == 0, \
+            lib.pp_last_error(ctx)
+        assert lib.pp_ctx_set_option(ctx, abi.PP_OPT_EXACT_ONLY, 1) == 0
+        try:
+            assert lib.pp_dpps_frames(ctx, frames, n, C.byref(p), C.byref(grid), kick,
+                                      exact) == 0, lib.pp_last_error(ctx)
+        finally:
+            lib.pp_ctx_set_option(ctx, abi.PP_OPT_EXACT_ONLY, 0)
+        assert bytes(fast) == bytes(exact)
+        for i in range(n):
+            st, blk = run_product(lib, ctx, frames[i], p, grid, kick[i], copy_all=False)
+            assert st == 0, lib.pp_last_error(ctx)
+            for r in range(3):
+                assert fast[i].best_cell[r] == blk.summary.best_cell[r], (i, r)
+                assert fast[i].best_score[r] == blk.summary.best_score[r], (i, r)
+                assert fast[i].n_feasible[r] == blk.summary.n_feasible[r], (i, r)
