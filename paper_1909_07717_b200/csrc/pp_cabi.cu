@@ -1523,6 +1523,14 @@ void pp_debug_scan_stats(unsigned long long* out16, int reset) {
     cudaMemcpyToSymbol(pp::g_scan_stats, z, sizeof(z));
   }
 }
+void pp_debug_act_hist(unsigned long long* out33, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out33, pp::g_act_hist, 33 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[33] = {};
+    cudaMemcpyToSymbol(pp::g_act_hist, z, sizeof(z));
+  }
+}
 #endif
 
 pp_status pp_scan_first(pp_ctx* ctx, int64_t n, const pp_scan_batch* batches,

@@ -443,6 +443,7 @@ __device__ __forceinline__ CellLane cell_window(const FrameDev& F, const DevPara
 // [24..39]: pairs by tests (bucket min(tests, 15) ... ), [40..55]: their tests;
 // [56]: lower-bound rejects in a run of >= 4 consecutive ones
 __device__ unsigned long long g_scan_stats[64];
+__device__ unsigned long long g_act_hist[33];  // warp steps by active lanes
 #define PP_STAT(i) atomicAdd(&g_scan_stats[i], 1ull)
 #define PP_STATN(i, n) atomicAdd(&g_scan_stats[i], static_cast<unsigned long long>(n))
 #else
@@ -804,6 +805,7 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
     if (lane == 0) {
       PP_STAT(12);
       PP_STATN(13, __popc(act));
+      atomicAdd(&g_act_hist[__popc(act)], 1ull);
       if (team) PP_STAT(23);  // their warp steps
     }
 #endif

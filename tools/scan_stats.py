@@ -18,6 +18,9 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 lib = abi.load_library()
 lib.pp_debug_scan_stats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 lib.pp_debug_scan_stats.restype = None
+lib.pp_debug_act_hist.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+lib.pp_debug_act_hist.restype = None
+hist = (C.c_ulonglong * 33)()
 ctx = C.c_void_p()
 assert lib.pp_ctx_create(0, C.byref(ctx)) == 0
 p = abi.Params()
@@ -28,9 +31,11 @@ for chip in (0, 1):
     fr, keep = synthetic.as_ctypes(synthetic.c5_frames(0, n))
     assert lib.pp_batch_upload(ctx, fr, n, None) == 0
     lib.pp_debug_scan_stats(st, 1)
+    lib.pp_debug_act_hist(hist, 1)
     ms = C.c_float()
     assert lib.pp_batch_run(ctx, C.byref(p), C.byref(g), C.byref(ms)) == 0
     lib.pp_debug_scan_stats(st, 1)
+    lib.pp_debug_act_hist(hist, 1)
     pairs = st[10]
     print(f"C5 batch {n} frames chip={chip}: pairs {pairs}")
     for i, nm in enumerate(NAMES):
@@ -48,3 +53,9 @@ for chip in (0, 1):
     print(f"  rest-rule arrivals {st[57] / pairs:.3f} per pair, {st[58] / max(st[57], 1):.3f} of them "
           f"<= t_stop, {st[59] / max(st[57], 1):.3f} ours")
     print(f"  lower-bound rejects in runs of >= 4: {st[56] / max(st[5], 1):.3f} of all lb rejects")
+    tot = sum(hist) or 1
+    print("  warp steps by active lanes (%):",
+          " ".join(f"{a}:{100 * hist[a] / tot:.1f}" for a in range(33) if hist[a]))
+    print("  lane-steps share of steps with <= 4 / <= 8 active lanes: "
+          f"{sum(a * hist[a] for a in range(5)) / max(sum(a * hist[a] for a in range(33)), 1):.3f} / "
+          f"{sum(a * hist[a] for a in range(9)) / max(sum(a * hist[a] for a in range(33)), 1):.3f}")
