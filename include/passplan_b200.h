@@ -360,6 +360,19 @@ pp_status pp_dpps_frames(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
                          const pp_params* params, const pp_search_grid* grid,
                          const int32_t* kicker_ids, pp_frame_summary* out);
 
+/* pp_dpps_frames over several devices from one process (SURVEY.md 8(b)3's
+ * pp_dpps_batch(per_gpu, n_gpu, ...) shape): frames split into n_ctx
+ * contiguous ranges, range i on ctxs[i] (one context per GPU; distinct
+ * contexts), all devices searching concurrently; out[i] is frame i's result
+ * as pp_dpps_frames gives it.  Errors: the first failing context's status;
+ * pp_last_error(ctxs[0]) names the context and the frame (index into
+ * `frames`).  Replaces the reference's frame loop over run_dpps + best_pass
+ * (passplan_main.cpp:87,102-104; dpps.cpp:217-321). */
+pp_status pp_dpps_frames_multi(pp_ctx* const* ctxs, int32_t n_ctx, const pp_world* frames,
+                               int64_t n_frames, const pp_params* params,
+                               const pp_search_grid* grid, const int32_t* kicker_ids,
+                               pp_frame_summary* out);
+
 /* Device-resident pieces of pp_dpps_frames, for benchmarking and pipelined
  * callers: pp_batch_upload copies the raw frames to HBM (asynchronously on
  * the context's stream); pp_batch_run stages them and runs the search on the

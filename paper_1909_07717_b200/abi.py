@@ -324,6 +324,8 @@ def _declare(lib):
     lib.pp_batch_download.argtypes = [vp, _P(FrameSummary)]
     lib.pp_dpps_frames.argtypes = [vp, _P(World), C.c_int64, _P(Params), _P(SearchGrid),
                                    _P(C.c_int32), _P(FrameSummary)]
+    lib.pp_dpps_frames_multi.argtypes = [_P(vp), C.c_int32, _P(World), C.c_int64, _P(Params),
+                                         _P(SearchGrid), _P(C.c_int32), _P(FrameSummary)]
     fp = _P(C.c_float)
     lib.pp_batch_kernel_times.argtypes = [vp, _P(Params), _P(SearchGrid), _I, fp, fp, fp,
                                           _P(C.c_int32)]
@@ -339,7 +341,7 @@ def _declare(lib):
     for fn in ("pp_params_validate", "pp_ctx_create", "pp_dpps", "pp_dpps_relaunch", "pp_score_cells",
                "pp_goal_views", "pp_runmap_count", "pp_runmap", "pp_dpps_batch",
                "pp_batch_upload", "pp_batch_run", "pp_batch_download", "pp_dpps_frames",
-               "pp_batch_kernel_times", "pp_intercept_all",
+               "pp_dpps_frames_multi", "pp_batch_kernel_times", "pp_intercept_all",
                "pp_possession", "pp_decide_shot", "pp_plan_free_kick"):
         getattr(lib, fn).restype = C.c_int
     return lib
@@ -368,7 +370,7 @@ EXPORTED_SYMBOLS = (
     "pp_host_free", "pp_dpps", "pp_dpps_relaunch", "pp_ctx_stream", "pp_dpps_kernel_times",
     "pp_grid_cells", "pp_score_cells", "pp_goal_views", "pp_runmap",
     "pp_dpps_batch", "pp_batch_upload", "pp_batch_run", "pp_batch_download", "pp_dpps_frames",
-    "pp_batch_kernel_times",
+    "pp_dpps_frames_multi", "pp_batch_kernel_times",
     "pp_score_running_points", "pp_kick_trajectory", "pp_intercept_all", "pp_possession",
     "pp_decide_shot", "pp_plan_free_kick", "pp_guard_points", "pp_scan_first",
 )

@@ -140,6 +140,7 @@ struct pp_ctx {
   DevBuf batch_worlds, batch_kick_in, batch_frames, batch_kickers, batch_bad, batch_rk;
   DevBuf batch_compact, batch_full;
   int64_t batch_n = 0;
+  int64_t batch_frame0 = 0;  // index of the first uploaded frame in the caller's array (messages)
   int batch_max_scan = 1;      // widest scan list of the uploaded frames
   bool batch_has_kickers = false;
   bool batch_ran = false;
@@ -1732,12 +1733,13 @@ pp_status batch_check(pp_ctx* ctx) {
   PP_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   if (bad == ~0ull) return PP_OK;
   const long long f = static_cast<long long>(bad >> 2);
+  const long long fg = f + ctx->batch_frame0;
   if ((bad & 3ull) == pp::kStageTeamSize)
-    return fail(ctx, PP_VALIDATION, "frame %lld: team size outside [0, 16]", f);
+    return fail(ctx, PP_VALIDATION, "frame %lld: team size outside [0, 16]", fg);
   int32_t kid = -1;
   PP_CUDA_TRY(ctx, cudaMemcpy(&kid, static_cast<const int32_t*>(ctx->batch_kickers.p) + f,
                               sizeof(kid), cudaMemcpyDeviceToHost));
-  return fail(ctx, PP_VALIDATION, "frame %lld: kicker id %d is not on team ours", f, kid);
+  return fail(ctx, PP_VALIDATION, "frame %lld: kicker id %d is not on team ours", fg, kid);
 }
 
 }  // namespace
@@ -1753,6 +1755,7 @@ pp_status pp_batch_upload(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
   PP_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   ctx->batch_ran = false;
   ctx->batch_n = n_frames;
+  ctx->batch_frame0 = 0;
   const size_t n = static_cast<size_t>(std::max<int64_t>(n_frames, 1));
   PP_CUDA_TRY(ctx, ctx->batch_worlds.reserve(ctx->stream, sizeof(pp_world) * n));
   PP_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->batch_worlds.p, frames, sizeof(pp_world) * n_frames,
@@ -1852,6 +1855,41 @@ pp_status pp_dpps_frames(pp_ctx* ctx, const pp_world* frames, int64_t n_frames,
   if (st == PP_OK) st = pp_batch_run(ctx, params, grid, nullptr);
   if (st == PP_OK) st = pp_batch_download(ctx, out);
   return st;
+}
+
+// One process, several devices (SURVEY 8(b)3's batch shape): contiguous
+// frame ranges, one per context; every context's upload and search are
+// enqueued before any result is read, so the devices run concurrently.
+pp_status pp_dpps_frames_multi(pp_ctx* const* ctxs, int32_t n_ctx, const pp_world* frames,
+                               int64_t n_frames, const pp_params* params,
+                               const pp_search_grid* grid, const int32_t* kicker_ids,
+                               pp_frame_summary* out) {
+  PP_NVTX("pp_dpps_frames_multi");
+  if (!ctxs || n_ctx < 1 || !ctxs[0]) return PP_INTERNAL;
+  pp_ctx* c0 = ctxs[0];
+  for (int i = 1; i < n_ctx; ++i)
+    if (!ctxs[i] || ctxs[i] == ctxs[i - 1])
+      return fail(c0, PP_INTERNAL, "context %d: null or repeated", i);
+  if ((!frames || !out) && n_frames > 0) return fail(c0, PP_INTERNAL, "null argument");
+  if (n_frames < 0) return fail(c0, PP_INTERNAL, "negative frame count");
+  auto lo = [&](int i) { return n_frames * i / n_ctx; };
+  auto relay = [&](int i, pp_status st) {  // the failing context's message, on ctxs[0]
+    if (i != 0) c0->err = "context " + std::to_string(i) + ": " + ctxs[i]->err;
+    return st;
+  };
+  for (int i = 0; i < n_ctx; ++i) {
+    const int64_t a = lo(i), m = lo(i + 1) - a;
+    pp_status st = pp_batch_upload(ctxs[i], frames + a, m, kicker_ids ? kicker_ids + a : nullptr);
+    ctxs[i]->batch_frame0 = a;
+    if (st == PP_OK) st = pp_batch_run(ctxs[i], params, grid, nullptr);
+    if (st != PP_OK) return relay(i, st);
+  }
+  pp_status first = PP_OK;
+  for (int i = 0; i < n_ctx; ++i) {  // (every context is drained, even after a failure)
+    const pp_status st = pp_batch_download(ctxs[i], out + lo(i));
+    if (st != PP_OK && first == PP_OK) first = relay(i, st);
+  }
+  return first;
 }
 
 // Full per-frame summaries (the single-frame pp_dpps_summary, best features

@@ -177,3 +177,46 @@ def test_run_sharded_product_runner_n1(ctx):
     got = run_sharded(frames_np, runner, 0, 1, row_type=abi.FrameSummary)
     want = runner(frames_np)
     assert bytes(got) == bytes(want)
+
+
+def test_frames_multi_contexts(ctx):
+    """pp_dpps_frames_multi (one process, one context per device; here 2 and
+    3 contexts on device 0): contiguous frame ranges per context, results
+    byte-identical to pp_dpps_frames on one context; a bad frame in a later
+    range is reported with its index into the caller's array."""
+    lib = abi.load_library()
+    p = _params()
+    n = 301
+    frames_np = np.concatenate([synthetic.c5_frames(0, 200), _mixed_frames(101, 9)])
+    frames, _keep = synthetic.as_ctypes(frames_np)
+    want = (abi.FrameSummary * n)()
+    assert lib.pp_dpps_frames(ctx, frames, n, C.byref(p), C.byref(C1), None, want) == 0
+    extra = []
+    try:
+        for _ in range(2):
+            c = C.c_void_p()
+            assert lib.pp_ctx_create(0, C.byref(c)) == 0
+            extra.append(c)
+        for k in (1, 2, 3):
+            ctxs = (C.c_void_p * k)(ctx, *extra[:k - 1])
+            got = (abi.FrameSummary * n)()
+            assert lib.pp_dpps_frames_multi(ctxs, k, frames, n, C.byref(p), C.byref(C1), None,
+                                            got) == 0, lib.pp_last_error(ctx)
+            assert bytes(got) == bytes(want), k
+        kick = (C.c_int32 * n)(*[int(frames_np["ours"]["id"][i][0]) for i in range(n)])
+        kick[250] = 77
+        ctxs = (C.c_void_p * 3)(ctx, *extra)
+        got = (abi.FrameSummary * n)()
+        assert lib.pp_dpps_frames_multi(ctxs, 3, frames, n, C.byref(p), C.byref(C1), kick,
+                                        got) == abi.PP_VALIDATION
+        msg = lib.pp_last_error(ctx).decode()
+        assert "context 2" in msg and "frame 250" in msg and "77" in msg, msg
+        # repeated contexts are refused; the contexts stay usable
+        assert lib.pp_dpps_frames_multi((C.c_void_p * 2)(ctx, ctx), 2, frames, n, C.byref(p),
+                                        C.byref(C1), None, got) == abi.PP_INTERNAL
+        assert lib.pp_dpps_frames_multi(ctxs, 3, frames, n, C.byref(p), C.byref(C1), None,
+                                        got) == 0
+        assert bytes(got) == bytes(want)
+    finally:
+        for c in extra:
+            lib.pp_ctx_destroy(c)
