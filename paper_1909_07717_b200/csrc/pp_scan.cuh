@@ -1483,6 +1483,7 @@ __device__ __forceinline__ void warp_tile(const FrameDev& F, const RobotK* rk_s,
   unsigned rest_mask = 0;  // robots (bit ri) whose pair ended without a hit
   for (int i = 0; i < F.n_scan; ++i) {
     const int ri = __ffs(__ballot_sync(0xffffffffu, my_rank == i)) - 1;
+    PP_CHECK(ri >= 0 && ri < F.n_scan);
     const RobotK& rk = rk_s[ri];
     const SampleF S = sample_f(rk, uf, P);
     double time;
@@ -1575,6 +1576,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtas)
     if (static_cast<int>(j) >= n_mine) break;
     const int b = g + groups * static_cast<int>(j);
     const int tile = kCells ? b : (b % per_pt) * P.n_ptiles + b / per_pt;
+    PP_CHECK(tile >= 0 && tile < P.n_tiles && (threadIdx.x >> 5) < kWarps);
     warp_tile<kCells>(sm.frame, sm.rk, ws, P, out, q, fc, f, tile);
   }
 }
