@@ -289,6 +289,17 @@ def run_reference(args, rank, world_size):
 # ---------------------------------------------------------------------------
 # GPU side.
 
+def _traffic_per_launch(n_frames, n_launches):
+    """ncu DRAM bytes of the dominant kernel per launch of this run: the
+    profiled per-frame traffic (profiles/ncu_summary.json, one ncu --set full
+    capture) x the frames one scan launch processes here."""
+    d = _load_json("profiles/ncu_summary.json")
+    per_frame = d.get("dram_bytes_per_frame")
+    if per_frame is None or n_launches < 1:
+        return d.get("dram_bytes_per_launch")
+    return per_frame * n_frames / n_launches
+
+
 def run_ours(args, rank, world_size, local_rank):
     import torch
     import torch.distributed as dist
@@ -472,8 +483,7 @@ def run_ours(args, rank, world_size, local_rank):
                                if world_size > 1 else "")},
             "roofline": {"bound": "fp32-core", "achieved": achieved, "peak": peak_tflops,
                          "unit": "TFLOP/s", "frac": achieved / peak_tflops,
-                         "traffic": _load_json("profiles/ncu_summary.json").get(
-                             "dram_bytes_per_launch"),
+                         "traffic": _traffic_per_launch(n_local, int(n_launch.value)),
                          "kernel": "scan_warp_kernel (SBIP search, batch shape: a warp per tile)",
                          "kernel_ms": {"stage+consts": stage_ms.value, "scan": scan_ms.value,
                                        "value (incl. score-bound pre-pass)": value_ms.value,

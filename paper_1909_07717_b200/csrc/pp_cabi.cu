@@ -1647,10 +1647,13 @@ cudaError_t enqueue_batch(pp_ctx* ctx, pp::DevParams P, pp_dpps_summary* full,
   cudaStream_t s = ctx->stream;
   const int64_t n_cells = static_cast<int64_t>(P.n_kt) * P.n_dirs * P.n_pows;
   // Frames are independent: launch them in groups so the per-frame cell
-  // queues stay a bounded working set (group x cells x 37 B).
+  // queues stay a bounded working set (group x cells x 37 B, at most 2^28
+  // cells = 9.9 GB of the 180 GB HBM).  Fewer, larger launches have fewer
+  // tails: C5 65,536 frames 359.6 ms in groups of 4,096, 355.3 (8,192),
+  // 352.0 (16,384), 350.5 (32,768 = the cell cap for the 128 x 64 grid).
   static const int64_t max_group = [] {
     const char* e = getenv("PP_BATCH_GROUP");  // dev knob
-    return e ? std::max<int64_t>(1, atoll(e)) : int64_t(4096);
+    return e ? std::max<int64_t>(1, atoll(e)) : int64_t(32768);
   }();
   int64_t group = (int64_t(1) << 28) / std::max<int64_t>(n_cells, 1);
   group = std::max<int64_t>(1, std::min<int64_t>(group, std::min<int64_t>(n, max_group)));
