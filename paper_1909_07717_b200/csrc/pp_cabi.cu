@@ -700,7 +700,7 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   // PP_WARP_CELLS=1 (single frames too).
   static const int warp_tiles = [] {
     const char* e = getenv("PP_WARP_TILES");
-    return e ? atoi(e) : 32;
+    return e ? atoi(e) : 128;
   }();
   static const bool warp_cells = [] {
     const char* e = getenv("PP_WARP_CELLS");
@@ -726,7 +726,14 @@ cudaError_t launch_pipeline(pp_ctx* ctx, const pp::FrameDev* frames, int64_t n_f
   }
   if (warp_tiles > 0 && (!kCells || warp_cells) &&
       sfn == pp::scan_kernel<kCells, pp::kScanWarpsNarrow, pp::kScanCtasNarrow>) {
-    Ps.scan_groups = std::max(1, P.n_tiles / warp_tiles);
+    // ~warp_tiles tiles per CTA (C5, 65,536 frames: 32 -> 350.6 ms, 64 ->
+    // 344.2, 128 -> 342.7, 256 -> 344.9), but at least ~8 waves of CTAs
+    // for smaller batches, and at least one tile per warp
+    const int64_t want = (8 * sms * pp::kScanWarpCtas + n_frames - 1) / n_frames;
+    int64_t groups = std::max<int64_t>(1, P.n_tiles / warp_tiles);
+    groups = std::min<int64_t>(std::max(groups, want),
+                               std::max<int64_t>(1, P.n_tiles / pp::kScanWarpWarps));
+    Ps.scan_groups = static_cast<int32_t>(groups);
     sfn = pp::scan_warp_kernel<kCells, pp::kScanWarpWarps, pp::kScanWarpCtas>;
     scfg.gridDim = dim3(static_cast<unsigned>(n_frames * Ps.scan_groups));
     scfg.blockDim = dim3(32 * pp::kScanWarpWarps);
