@@ -1648,6 +1648,9 @@ struct BatchTimes {
   int n_scan_launches = 0;
 };
 
+#ifndef PP_BATCH_CELLS_LOG2
+#define PP_BATCH_CELLS_LOG2 28
+#endif
 cudaError_t enqueue_batch(pp_ctx* ctx, pp::DevParams P, pp_dpps_summary* full,
                           BatchTimes* times) {
   const int64_t n = ctx->batch_n;
@@ -1662,7 +1665,7 @@ cudaError_t enqueue_batch(pp_ctx* ctx, pp::DevParams P, pp_dpps_summary* full,
     const char* e = getenv("PP_BATCH_GROUP");  // dev knob
     return e ? std::max<int64_t>(1, atoll(e)) : int64_t(32768);
   }();
-  int64_t group = (int64_t(1) << 28) / std::max<int64_t>(n_cells, 1);
+  int64_t group = (int64_t(1) << PP_BATCH_CELLS_LOG2) / std::max<int64_t>(n_cells, 1);
   group = std::max<int64_t>(1, std::min<int64_t>(group, std::min<int64_t>(n, max_group)));
   cudaError_t e = reserve_pipeline(ctx, P, group);
   if (e == cudaSuccess)
