@@ -25,6 +25,9 @@ constexpr int kScanWarpsWide = 16, kScanCtasWide = 2;
 #endif
 constexpr int kScanWarpsNarrow = PP_SCAN_WARPS_NARROW, kScanCtasNarrow = PP_SCAN_CTAS_NARROW;
 constexpr int kScanWarpsMid = 8, kScanCtasMid = 4;  // one wave of up to 4 x 148 tiles
+#ifndef PP_TILE_PRUNE
+#define PP_TILE_PRUNE 1
+#endif
 #ifndef PP_SCAN_WARP_W
 #define PP_SCAN_WARP_W 4
 #endif
@@ -33,6 +36,7 @@ constexpr int kScanWarpsMid = 8, kScanCtasMid = 4;  // one wave of up to 4 x 148
 #endif
 // scan_warp_kernel (batches): warps per CTA and CTAs per SM
 constexpr int kScanWarpWarps = PP_SCAN_WARP_W, kScanWarpCtas = PP_SCAN_WARP_C;
+constexpr bool kTilePrune = PP_TILE_PRUNE != 0;  // warp-tile scan: per-tile robot prune
 #ifndef PP_VALUE_CHUNK
 #define PP_VALUE_CHUNK 32
 #endif
@@ -1458,6 +1462,38 @@ __device__ __forceinline__ void warp_tile(const FrameDev& F, const RobotK* rk_s,
       my_rank += (kj < key || (kj == key && j < lane)) ? 1 : 0;
     }
   }
+  // Robots no cell of the tile can need: scan_start's window prune (the
+  // quick reject over the whole window, intercept.cpp:89-95, in FP32 with
+  // 1 mm of slack) applied to the union of the cells' windows -- the segment
+  // from the nearest first sample to the farthest last one, the latest last
+  // sample time -- so it prunes only robots every cell's own prune drops.
+  // One pass with lane = robot instead of a scan per robot.
+  unsigned pruned = 0u;
+  if (kTilePrune && !P.exact_only) {
+    const bool has = c.valid && c.kb < c.ke;
+    float lo = has ? ws.win_s[lane].x : 3.0e38f;
+    float hi = has ? ws.win_s[lane].y : -3.0e38f;
+    float tk = has ? static_cast<float>(c.ke - 1) * P.dtf : 0.f;
+    for (int sh = 16; sh > 0; sh >>= 1) {
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, sh));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, sh));
+      tk = fmaxf(tk, __shfl_xor_sync(0xffffffffu, tk, sh));
+    }
+    bool drop = false;
+    if (lane < F.n_scan) {
+      if (hi < lo) {
+        drop = true;  // no cell has a window
+      } else {
+        const RobotK& rk = rk_s[lane];
+        const float s0 = -(rk.bxf * uf.x + rk.byf * uf.y);
+        const float sc = fminf(fmaxf(s0, lo), hi);
+        const float ex = fmaf(uf.x, sc, rk.bxf), ey = fmaf(uf.y, sc, rk.byf);
+        const float gap = sqrt_a(ex * ex + ey * ey) - 1e-3f - P.radf;
+        drop = gap > rk.vbf * tk * 1.0001f;
+      }
+    }
+    pruned = __ballot_sync(0xffffffffu, drop);
+  }
   // B: every robot in rank order, this lane's champions -- (time bits, id)
   // argmin per team, as tile_champions -- updated after each
   unsigned long long bt_o = 0x7ff0000000000000ull, bt_t = 0x7ff0000000000000ull;  // +inf
@@ -1484,6 +1520,10 @@ __device__ __forceinline__ void warp_tile(const FrameDev& F, const RobotK* rk_s,
   for (int i = 0; i < F.n_scan; ++i) {
     const int ri = __ffs(__ballot_sync(0xffffffffu, my_rank == i)) - 1;
     PP_CHECK(ri >= 0 && ri < F.n_scan);
+    if ((pruned >> ri) & 1u) {  // every cell's window pruned: no hit, rest rule
+      if (c.valid && c.rif) rest_mask |= 1u << ri;
+      continue;
+    }
     const RobotK& rk = rk_s[ri];
     const SampleF S = sample_f(rk, uf, P);
     double time;
