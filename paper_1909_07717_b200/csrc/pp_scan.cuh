@@ -694,7 +694,10 @@ __device__ __forceinline__ int scan_start(const CellLane& c, const SampleF& S, f
   if (gap > S.vbf * static_cast<float>(ke - 1) * S.dtf * 1.0001f) return ke;
   int k = kb;
   if (S.vbf > 0.f && gap > 0.f) {
-    const int kk = static_cast<int>(floorf(gap / (S.vbf * S.dtf * 1.0001f))) - 1;
+    // (approximate reciprocal, ~2 ulp; the 1e-6 shrink keeps the quotient
+    // at or below the exact one, so the start is never later)
+    const int kk =
+        static_cast<int>(floorf(gap * rcp_ftz(S.vbf * S.dtf * 1.0001f) * (1.f - 1e-6f))) - 1;
     k = kk > kb ? (kk < ke ? kk : ke) : kb;
   }
   return k;
