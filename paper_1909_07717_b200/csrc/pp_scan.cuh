@@ -489,11 +489,14 @@ __device__ __forceinline__ SampleF sample_f(const RobotK& rk, float2 uf, const D
 __device__ __forceinline__ int test_sample(const RobotK& rk, const SampleF& S, int kk,
                                            const TrajF& tf_, int ke_s, int cap_c, int* next) {
   PP_STAT(0);
-  if (kk >= ke_s) {
-    PP_STAT(1);
-    return kEnd;
-  }
-  if (kk > cap_c) {
+  // one compare against min(window end, cap + 1) (loop-invariant in a robot's
+  // scan), then which of the two it was
+  const int lim = cap_c < ke_s ? cap_c + 1 : ke_s;
+  if (kk >= lim) {
+    if (kk >= ke_s) {
+      PP_STAT(1);
+      return kEnd;
+    }
     PP_STAT(2);
     return kCap;
   }
