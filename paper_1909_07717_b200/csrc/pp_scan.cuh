@@ -517,7 +517,8 @@ __device__ __forceinline__ int test_sample(const RobotK& rk, const SampleF& S, i
     const float approach = sf < S.s0 + 1e-3f ? tf_.speed_at(tf) : 0.f;
     const float rate = (approach + S.vbf) * S.dtf * 1.0001f;
     const float j = floorf(gap * rcp_ftz(rate) * 0.9999f);
-    *next = kk + 1 + (j > 1.f ? (j < 4096.f ? static_cast<int>(j) - 1 : 4095) : 0);
+    // skip j - 1 samples, clamped to [0, 4095] (NaN: 0)
+    *next = kk + 1 + static_cast<int>(fminf(fmaxf(j - 1.f, 0.f), 4095.f));
     PP_STAT(3);
     PP_STATN(4, *next - kk - 1);
     return kRej;
