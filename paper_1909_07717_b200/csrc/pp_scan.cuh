@@ -37,6 +37,10 @@ constexpr int kScanWarpsMid = 8, kScanCtasMid = 4;  // one wave of up to 4 x 148
 // scan_warp_kernel (batches): warps per CTA and CTAs per SM
 constexpr int kScanWarpWarps = PP_SCAN_WARP_W, kScanWarpCtas = PP_SCAN_WARP_C;
 constexpr bool kTilePrune = PP_TILE_PRUNE != 0;  // warp-tile scan: per-tile robot prune
+#ifndef PP_REST_LB
+#define PP_REST_LB 1
+#endif
+constexpr bool kRestLB = PP_REST_LB != 0;  // warp-tile scan: rest rule behind a lower bound
 #ifndef PP_VALUE_CHUNK
 #define PP_VALUE_CHUNK 32
 #endif
@@ -1561,6 +1565,22 @@ __device__ __forceinline__ void warp_tile(const FrameDev& F, const RobotK* rk_s,
           (kX && !theirs && cap_t != 0x7fffffff &&
            c.tr.t_stop + xd(P.safety) > xd(double(cap_t)) * xd(P.dt)))
         continue;
+      if (kRestLB && !P.exact_only) {
+        // the FP32 arrival lower bound at the rest point (the sample test's
+        // ArrivalLB): above the team's champion time, this robot's rest-rule
+        // time max(arrival, t_stop) can neither beat nor tie it
+        const unsigned long long bt = theirs ? bt_t : bt_o;
+        if (bt != 0x7ff0000000000000ull) {
+          const RobotK& rk = rk_s[rj];
+          const float ds = static_cast<float>(c.tr.d_stop.v);
+          const float qx = fmaf(uf.x, ds, rk.bxf), qy = fmaf(uf.y, ds, rk.byf);
+          const float d2 = fmaf(qx, qx, qy * qy);
+          const float inv = rsqrt_ftz(fmaxf(d2, 1e-30f));
+          if (static_cast<double>(rk.lb.lower_bound(qx, qy, d2 * inv, inv, P.radf)) >
+              __longlong_as_double(static_cast<long long>(bt)))
+            continue;
+        }
+      }
       double t;
       int cd;
       pair_result(c, P, robot_x(F, P, rk_s[rj], rj), -1, false, &t, &cd);
