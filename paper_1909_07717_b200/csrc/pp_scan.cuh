@@ -37,6 +37,9 @@ constexpr int kScanWarpsMid = 8, kScanCtasMid = 4;  // one wave of up to 4 x 148
 // scan_warp_kernel (batches): warps per CTA and CTAs per SM
 constexpr int kScanWarpWarps = PP_SCAN_WARP_W, kScanWarpCtas = PP_SCAN_WARP_C;
 constexpr bool kTilePrune = PP_TILE_PRUNE != 0;  // warp-tile scan: per-tile robot prune
+#ifndef PP_REST_RANK
+#define PP_REST_RANK 1  // warp-tile scan: rest rule in rank order (dev knob)
+#endif
 #ifndef PP_REST_LB
 #define PP_REST_LB 1
 #endif
@@ -1419,6 +1422,7 @@ struct WarpTile {
   TrajF trf[32];
   float2 win_s[32];
   int32_t cap[3][32];  // team caps (ours, theirs) and our cross cap, per cell
+  int8_t order[32];    // the tile's robots by rank
 };
 
 
@@ -1527,12 +1531,21 @@ __device__ __forceinline__ void warp_tile(const FrameDev& F, const RobotK* rk_s,
     }
   };
   constexpr bool kX = !kCells && kCrossCap;
-  unsigned rest_mask = 0;  // robots (bit ri) whose pair ended without a hit
+#if PP_REST_RANK
+  // robots (bit = rank) whose pair ended without a hit: the rest rule runs
+  // nearest first, so the champion it sets early filters the others
+  if (my_rank < F.n_scan) ws.order[my_rank] = static_cast<int8_t>(lane);
+  __syncwarp();
+#define PP_REST_BIT(i, ri) (1u << (i))
+#else
+#define PP_REST_BIT(i, ri) (1u << (ri))
+#endif
+  unsigned rest_mask = 0;  // robots whose pair ended without a hit
   for (int i = 0; i < F.n_scan; ++i) {
     const int ri = __ffs(__ballot_sync(0xffffffffu, my_rank == i)) - 1;
     PP_CHECK(ri >= 0 && ri < F.n_scan);
     if ((pruned >> ri) & 1u) {  // every cell's window pruned: no hit, rest rule
-      if (c.valid && c.rif) rest_mask |= 1u << ri;
+      if (c.valid && c.rif) rest_mask |= PP_REST_BIT(i, ri);
       continue;
     }
     const RobotK& rk = rk_s[ri];
@@ -1544,7 +1557,7 @@ __device__ __forceinline__ void warp_tile(const FrameDev& F, const RobotK* rk_s,
     if (code >= 0) {
       champion(ri, time, code);
     } else if (code == kNoHit && c.valid && c.rif) {
-      rest_mask |= 1u << ri;
+      rest_mask |= PP_REST_BIT(i, ri);
     }
     // (capped out, or no hit with the rest outside the field: +inf, which
     // never displaces a champion)
@@ -1557,7 +1570,11 @@ __device__ __forceinline__ void warp_tile(const FrameDev& F, const RobotK* rk_s,
   {
     const int cap_o = ws.cap[0][lane], cap_t = ws.cap[1][lane];
     while (rest_mask) {
+#if PP_REST_RANK
+      const int rj = ws.order[__ffs(rest_mask) - 1];
+#else
       const int rj = __ffs(rest_mask) - 1;
+#endif
       rest_mask &= rest_mask - 1;
       const bool theirs = F.scan_slot[rj] >= kTheirs;
       const int k_team = theirs ? cap_t : cap_o;
