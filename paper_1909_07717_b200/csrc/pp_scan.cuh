@@ -40,6 +40,10 @@ constexpr bool kTilePrune = PP_TILE_PRUNE != 0;  // warp-tile scan: per-tile rob
 #ifndef PP_REST_RANK
 #define PP_REST_RANK 1  // warp-tile scan: rest rule in rank order (dev knob)
 #endif
+#ifndef PP_REST_X
+#define PP_REST_X 1
+#endif
+constexpr bool kRestX = PP_REST_X != 0;  // batches: our rest rules behind their champion too
 #ifndef PP_REST_LB
 #define PP_REST_LB 1
 #endif
@@ -1587,14 +1591,21 @@ __device__ __forceinline__ void warp_tile(const FrameDev& F, const RobotK* rk_s,
         // ArrivalLB): above the team's champion time, this robot's rest-rule
         // time max(arrival, t_stop) can neither beat nor tie it
         const unsigned long long bt = theirs ? bt_t : bt_o;
-        if (bt != 0x7ff0000000000000ull) {
+        // batches, ours: their champion so far ends the cell's chances once
+        // fl(bound + safety) > it (dpps.cpp:207-212) -- then this robot is
+        // not the champion of a feasible cell
+        const bool vs_theirs = kX && kRestX && !theirs && bt_t != 0x7ff0000000000000ull;
+        if (bt != 0x7ff0000000000000ull || vs_theirs) {
           const RobotK& rk = rk_s[rj];
           const float ds = static_cast<float>(c.tr.d_stop.v);
           const float qx = fmaf(uf.x, ds, rk.bxf), qy = fmaf(uf.y, ds, rk.byf);
           const float d2 = fmaf(qx, qx, qy * qy);
           const float inv = rsqrt_ftz(fmaxf(d2, 1e-30f));
-          if (static_cast<double>(rk.lb.lower_bound(qx, qy, d2 * inv, inv, P.radf)) >
-              __longlong_as_double(static_cast<long long>(bt)))
+          const double lbd =
+              static_cast<double>(rk.lb.lower_bound(qx, qy, d2 * inv, inv, P.radf));
+          if (lbd > __longlong_as_double(static_cast<long long>(bt))) continue;
+          if (vs_theirs &&
+              (xd(lbd) + xd(P.safety)).v > __longlong_as_double(static_cast<long long>(bt_t)))
             continue;
         }
       }
