@@ -40,6 +40,9 @@ constexpr bool kTilePrune = PP_TILE_PRUNE != 0;  // warp-tile scan: per-tile rob
 #ifndef PP_REST_RANK
 #define PP_REST_RANK 1  // warp-tile scan: rest rule in rank order (dev knob)
 #endif
+#ifndef PP_EARLY_CAP
+#define PP_EARLY_CAP 1
+#endif
 #ifndef PP_REST_X
 #define PP_REST_X 1
 #endif
@@ -821,6 +824,14 @@ __device__ __forceinline__ void scan_robot(const CellLane& c, const TrajF& trf_i
     }
   };
   const int cap_solo = kSolo ? (kX ? min(*vcap, *vxcap) : *vcap) : 0;
+#if PP_EARLY_CAP
+  // solo scans: a start already past the (fixed) cap ends as the first
+  // test would (kCap), before the loop
+  if (kSolo && state == 0 && k > cap_solo) {
+    capped = true;
+    state = 2;
+  }
+#endif
   for (int n_step = 0; n_step < max_steps; ++n_step) {
     const unsigned act = __ballot_sync(0xffffffffu, state == 0);
 #ifdef PP_SCAN_STATS
