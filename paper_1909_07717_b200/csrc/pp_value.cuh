@@ -338,7 +338,10 @@ __device__ __forceinline__ void value_chunk(ValueSmem& sm, const DevParams& P, c
 // FrameCounters::lb_key -- value_chunk then drops every cell whose upper
 // bound is below its slot's key before the goal view (it cannot be the
 // slot's best_pass).  The queue is complete: this grid runs after the scan.
-__global__ void __launch_bounds__(256) score_lb_kernel(const FrameDev* __restrict__ frames,
+#ifndef PP_SCORE_LB_MINB
+#define PP_SCORE_LB_MINB 4  // 64 registers: 4 CTAs/SM (C5 -1.5 % against 128 registers, 2 CTAs)
+#endif
+__global__ void __launch_bounds__(256, PP_SCORE_LB_MINB) score_lb_kernel(const FrameDev* __restrict__ frames,
                                                        DevParams P, CellQueue q,
                                                        FrameCounters* __restrict__ fc,
                                                        int64_t n_frames) {
