@@ -211,6 +211,12 @@ def test_frames_multi_contexts(ctx):
                                         got) == abi.PP_VALIDATION
         msg = lib.pp_last_error(ctx).decode()
         assert "context 2" in msg and "frame 250" in msg and "77" in msg, msg
+        # fewer frames than contexts (some ranges empty), and no frames
+        for m in (2, 1, 0):
+            few = (abi.FrameSummary * max(m, 1))()
+            assert lib.pp_dpps_frames_multi(ctxs, 3, frames, m, C.byref(p), C.byref(C1), None,
+                                            few) == 0, lib.pp_last_error(ctx)
+            assert bytes(few)[:48 * m] == bytes(want)[:48 * m]
         # repeated contexts are refused; the contexts stay usable
         assert lib.pp_dpps_frames_multi((C.c_void_p * 2)(ctx, ctx), 2, frames, n, C.byref(p),
                                         C.byref(C1), None, got) == abi.PP_INTERNAL
